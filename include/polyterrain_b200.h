@@ -1,0 +1,206 @@
+/*
+ * polyterrain_b200.h — C-ABI of the B200-native fBm heightmap path.
+ *
+ * This is the drop-in boundary for the reference's generator API
+ * (/root/reference/proj/include/terrain/fbm.hpp:538-685) and the fractal
+ * analysis pass after it (terrain/analysis.hpp:213-305).  Every entry point
+ * takes plain pointers and sizes; device pointers are CUDA global memory and
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ * Device entry points are asynchronous and stream-ordered unless stated.
+ *
+ * Status codes mirror terrain/errors.hpp:9-36:
+ *   TG_OK          0  success
+ *   TG_EVALIDATION 1  terrain::ValidationError   (bad argument / config)
+ *   TG_EIO         2  terrain::IoError
+ *   TG_ENUMERICAL  3  terrain::NumericalError
+ *   TG_EDEVICE     4  CUDA / device failure (std::runtime_error in the C++ mirror)
+ * tg_last_error() returns the thread-local message of the last failure.
+ *
+ * The library has no CPU fallback: every compute entry point launches CUDA
+ * kernels built for sm_100a and fails with TG_EDEVICE when no device exists.
+ */
+#ifndef POLYTERRAIN_B200_H
+#define POLYTERRAIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+
+enum tg_status {
+    TG_OK = 0,
+    TG_EVALIDATION = 1,
+    TG_EIO = 2,
+    TG_ENUMERICAL = 3,
+    TG_EDEVICE = 4
+};
+
+/* terrain::fbm::Method, same order (fbm.hpp:27). */
+enum tg_method {
+    TG_METHOD_ZG_PAPER = 0,
+    TG_METHOD_ZG_SEPARABLE = 1,
+    TG_METHOD_GENERIC = 2,
+    TG_METHOD_PERLIN3 = 3,
+    TG_METHOD_PERLIN5 = 4
+};
+
+/* Lifted caps: the reference caps resolution and extent at
+ * 16384 (fbm.hpp:74,547); the B200 path accepts 32768^2 terrains and more. */
+#define TG_MAX_RESOLUTION (1LL << 22)
+#define TG_MAX_EXTENT (1LL << 17)
+#define TG_MAX_OCTAVES 32
+
+/* Lattice output lanes (lattice.hpp:53-54); lane 0 = corner height. */
+#define TG_LANE_HEIGHT 0ULL
+#define TG_LANE_ANGLE 0xA0761D6478BD642FULL
+#define TG_LANE_MAGNITUDE 0xE7037ED1A0B428DBULL
+/* 3D key extension (new): pack3 = pack2 + (u64)iz * K5,
+ * so iz = 0 reproduces the 2D lattice exactly. */
+#define TG_PACK_K5 0xA24BAED4963EE407ULL
+
+/*
+ * Mirror of terrain::fbm::FbmConfig (fbm.hpp:49-89) plus the fields the
+ * reference cannot express: an explicit smoothstep order and
+ * the ZeroSource test hook (fbm.hpp:125-133).
+ */
+typedef struct tg_fbm_config {
+    uint64_t seed;
+    int32_t method;            /* enum tg_method */
+    int32_t smoothstep;        /* 0 = reference default (S5 for perlin5, else S3); or 3 / 5 */
+    int32_t octaves;           /* [1, 32] */
+    int32_t threads;           /* validated [0, 256] like the reference, ignored on device */
+    int64_t resolution;        /* [1, TG_MAX_RESOLUTION] */
+    int64_t base_frequency;    /* cells across the map at octave 0, [1, TG_MAX_RESOLUTION] */
+    double frequency_ratio;    /* > 1 */
+    double persistence;        /* (0, 1] */
+    double base_amplitude;     /* > 0 */
+    double gradient_weight;    /* generic kernel only; read when has_gradient_weight != 0 */
+    int32_t has_gradient_weight; /* 0 = std::nullopt -> base_amplitude / 100 (fbm.hpp:62-64) */
+    int32_t normalize;         /* generate_heightmap/region rescale to [-1, 1] (fbm.hpp:668) */
+    int32_t zero_lattice;      /* 1 = ZeroSource: every corner datum is 0 */
+    int32_t reserved;
+} tg_fbm_config;
+
+/* terrain::fbm::detail::OctaveSpec (fbm.hpp:143-168). */
+typedef struct tg_octave_spec {
+    double freq;
+    double amp;
+    int32_t fast;    /* integer cell count dividing the resolution */
+    int32_t ppc;     /* pixels per cell, valid when fast */
+    int64_t cells;   /* valid when fast */
+} tg_octave_spec;
+
+/* terrain::lattice::LatticeKey (lattice.hpp:16-21); iz is the 3D extension. */
+typedef struct tg_lattice_key {
+    uint64_t seed;
+    uint32_t octave;
+    uint32_t pad;
+    int64_t ix;
+    int64_t iy;
+} tg_lattice_key;
+
+/* ---- library / host logic (no device needed) ---------------------------- */
+
+int tg_abi_version(void);
+const char* tg_last_error(void);
+/* FbmConfig::validate (fbm.hpp:71-88) with the lifted caps. */
+int tg_fbm_validate(const tg_fbm_config* cfg);
+/* detail::octave_spec (fbm.hpp:151-168). */
+int tg_fbm_octave_spec(const tg_fbm_config* cfg, int32_t octave, tg_octave_spec* out);
+/* The window checks of generate_into_with_source (fbm.hpp:546-558). */
+int tg_fbm_validate_window(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
+                           int64_t height);
+/* Number of visible CUDA devices (0 when none); never launches a kernel. */
+int tg_device_count(void);
+
+/* ---- generation (replaces fbm::generate_into_with_source, fbm.hpp:541-628) */
+
+/* Square window [ox, ox+extent) x [oy, oy+extent) into dev_out (n_out must
+ * equal extent^2, row-major [y*extent + x], fp32).  Stream-ordered. */
+int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                        float* dev_out, uint64_t n_out, void* stream);
+/* Rectangular window with a row pitch (elements); used for row bands and
+ * chunk grids.  Same per-pixel values as the square form (pure function of
+ * the global pixel). */
+int tg_fbm_generate_rect_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
+                             int64_t height, float* dev_out, int64_t ld, void* stream);
+/* A batch of maps that differ only in seed: out[b] is the window for
+ * seeds[b] (host array), contiguous maps of width*height.  One launch. */
+int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, int32_t n_seeds,
+                              int64_t ox, int64_t oy, int64_t width, int64_t height,
+                              float* dev_out, void* stream);
+/* Drop-in for generate_into(cfg, origin, extent, std::span<double>): host
+ * buffer of extent^2 doubles, synchronous.  Device work is fp32; the result
+ * is widened on the device and copied back in pipelined row bands. */
+int tg_fbm_generate_f64_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                             double* host_out, uint64_t n_out);
+/* Same, fp32 host buffer (pinned or pageable), synchronous. */
+int tg_fbm_generate_f32_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                             float* host_out, uint64_t n_out);
+
+/* 3D fBm volume (new): separable zero-gradient cells
+ * (method TG_METHOD_ZG_SEPARABLE only), layout [(z*ny + y)*nx + x]. */
+int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t oz,
+                          int64_t nx, int64_t ny, int64_t nz, float* dev_out, void* stream);
+
+/* ---- lattice (lattice.hpp:35-83) ------------------------------------------ */
+
+/* out[i] = mix(pack(keys[i]) ^ lane), bit-exact u64.  keys/out are device. */
+int tg_lattice_hash(const tg_lattice_key* dev_keys, uint64_t n, uint64_t lane,
+                    uint64_t* dev_out, void* stream);
+/* out[i] = float(corner_height(keys[i])) rounded to nearest. */
+int tg_lattice_height_f32(const tg_lattice_key* dev_keys, uint64_t n, float* dev_out,
+                          void* stream);
+/* out[2i..2i+1] = corner_unit_gradient (fp32 cos/sin of the hashed angle). */
+int tg_lattice_unit_gradient_f32(const tg_lattice_key* dev_keys, uint64_t n, float* dev_out,
+                                 void* stream);
+
+/* ---- normalization (fbm.hpp:638-656) -------------------------------------- */
+
+/* Device min/max of n floats; results written to host doubles; synchronous. */
+int tg_minmax_f32(const float* dev_map, uint64_t n, double* out_min, double* out_max,
+                  void* stream);
+/* In-place affine rescale to [-1, 1] with the given source range. */
+int tg_rescale_f32(float* dev_map, uint64_t n, double lo, double hi, void* stream);
+
+/* ---- fractal analysis (analysis.hpp:213-305; variogram new) --------------- */
+
+/* Upper median (element n/2 of the sorted map, analysis.hpp:244-250) by
+ * radix select on the device; synchronous, result to host. */
+int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* stream);
+/* coastline_mask (analysis.hpp:213-240): dev_mask[i] = 1 for land pixels
+ * (h >= sea) with a 4-neighbour water pixel; land count to host.
+ * Synchronous. */
+int tg_coastline_mask(const float* dev_map, int64_t resolution, double sea_level,
+                      uint8_t* dev_mask, int64_t* out_land_count, void* stream);
+/* Fused coastline + box count (analysis.hpp:213-240 + 269-299): occupied
+ * box counts for each size (host arrays), plus coast pixel and land counts.
+ * Synchronous. */
+int tg_coastline_boxcount(const float* dev_map, int64_t resolution, double sea_level,
+                          const int32_t* sizes, int32_t n_sizes, int64_t* out_counts,
+                          int64_t* out_coast_pixels, int64_t* out_land_count, void* stream);
+/* Box counts of an explicit u8 mask (box_count on a CoastlineMask). */
+int tg_boxcount_mask(const uint8_t* dev_mask, int64_t resolution, const int32_t* sizes,
+                     int32_t n_sizes, int64_t* out_counts, void* stream);
+/* Height-difference variogram: for each lag h in lags (host array) and axis
+ * (0 = x, 1 = y): sum_sq[2*i+axis] = sum over in-window pairs of
+ * (z(p + h e_axis) - z(p))^2 accumulated in fp64, pairs[2*i+axis] = pair
+ * count.  Window is width x height with row pitch ld.  Synchronous. */
+int tg_variogram_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld,
+                     const int32_t* lags, int32_t n_lags, double* out_sum_sq,
+                     int64_t* out_pairs, void* stream);
+
+/* ---- measurement helpers ---------------------------------------------------- */
+
+/* FP32 FFMA-chain peak on the current device (TFLOP/s), for the roofline
+ * denominator; synchronous. */
+int tg_measure_ffma_peak(double* out_tflops, double* out_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POLYTERRAIN_B200_H */
