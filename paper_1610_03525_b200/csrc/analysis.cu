@@ -1,0 +1,441 @@
+// analysis.cu — the fractal-analysis pass after generation.
+//
+//   upper median      analysis.hpp:244-250 (nth_element at n/2) -> 3-pass radix select
+//   coastline_mask    analysis.hpp:213-240 -> warp-ballot bit mask (1 bit/pixel)
+//   box_count         analysis.hpp:269-299 -> per-box OR over the bit mask, popcount
+//   variogram         new (BASELINE.json config 5): fp64-accumulated block reduction
+// All integer results (median element, mask bits, land/coast/box counts) are
+// exact, so they equal the reference run on the same fp32 map.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "../../include/polyterrain_b200.h"
+
+namespace tg {
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t e, const char* where);
+int check_device();
+
+namespace {
+
+__device__ __forceinline__ uint32_t fkey(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// ---- radix select -------------------------------------------------------------
+struct SelectState {
+    uint32_t prefix;  // selected high bits so far
+    uint32_t mask;    // which bits of the key are fixed
+    uint64_t k;       // rank still to find within the matching elements
+};
+
+constexpr int kBins = 2048;
+
+__global__ void radix_hist(const float* __restrict__ x, uint64_t n, const SelectState* st,
+                           int shift, int bits, unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[kBins];
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint32_t prefix = st->prefix, mask = st->mask;
+    const uint32_t dmask = (1u << bits) - 1u;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t key = fkey(x[i]);
+        if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(sh[i]));
+}
+
+__global__ void radix_pick(SelectState* st, unsigned long long* hist, int shift, int bits) {
+    if (threadIdx.x != 0) return;
+    const int nb = 1 << bits;
+    uint64_t k = st->k, acc = 0;
+    int b = 0;
+    for (; b < nb; ++b) {
+        if (acc + hist[b] > k) break;
+        acc += hist[b];
+    }
+    st->k = k - acc;
+    st->prefix |= static_cast<uint32_t>(b) << shift;
+    st->mask |= static_cast<uint32_t>(nb - 1) << shift;
+    for (int i = 0; i < nb; ++i) hist[i] = 0;
+}
+
+// ---- coastline bit mask -------------------------------------------------------
+// One warp per 1024-pixel row segment (32 words).  coast = land & !(all four
+// neighbours land), neighbours outside the map count as land (the reference
+// only tests in-bounds neighbours).
+__global__ void coast_bits_kernel(const float* __restrict__ h, int64_t R, float sea,
+                                  uint32_t* __restrict__ bits, uint8_t* __restrict__ mask8,
+                                  unsigned long long* __restrict__ counts /* land, coast */) {
+    const int64_t words = (R + 31) / 32;
+    const int64_t segs = (words + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_global = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long land = 0, coast = 0;
+    for (int64_t t = warp_global; t < R * segs; t += nwarps) {
+        const int64_t y = t / segs;
+        const int64_t w0 = (t - y * segs) * 32;
+        const float* row = h + y * R;
+        const float* up = y > 0 ? row - R : nullptr;
+        const float* dn = y + 1 < R ? row + R : nullptr;
+        // land bits of this row and the neighbours, one word per iteration;
+        // lane i ends up owning word w0 + i.
+        uint32_t Lc = 0, Lu = 0, Ld = 0;
+        for (int i = 0; i < 32; ++i) {
+            const int64_t w = w0 + i;
+            if (w >= words) break;
+            const int64_t x = w * 32 + lane;
+            const bool in = x < R;
+            const bool c = in && row[x] >= sea;
+            const bool u = !in || !up || up[x] >= sea;
+            const bool d = !in || !dn || dn[x] >= sea;
+            const uint32_t bc = __ballot_sync(0xffffffffu, c);
+            const uint32_t bu = __ballot_sync(0xffffffffu, u);
+            const uint32_t bd = __ballot_sync(0xffffffffu, d);
+            if (lane == i) {
+                Lc = bc;
+                Lu = bu;
+                Ld = bd;
+            }
+        }
+        const int64_t w = w0 + lane;
+        // horizontal neighbours: bit b-1 / b+1 incl. the adjacent words' edge bits
+        const uint32_t prev = __shfl_up_sync(0xffffffffu, Lc, 1);
+        const uint32_t next = __shfl_down_sync(0xffffffffu, Lc, 1);
+        if (w < words) {
+            uint32_t prev_hi, next_lo;
+            if (lane == 0)
+                prev_hi = w == 0 ? 1u : (row[w * 32 - 1] >= sea ? 1u : 0u);
+            else
+                prev_hi = prev >> 31;
+            if (lane == 31 || w + 1 >= words)
+                next_lo = (w + 1) * 32 >= R ? 1u : (row[(w + 1) * 32] >= sea ? 1u : 0u);
+            else
+                next_lo = next & 1u;
+            const int64_t valid = R - w * 32;  // bits beyond R count as land
+            const uint32_t beyond = valid >= 32 ? 0u : ~((1u << valid) - 1u);
+            const uint32_t Lr = (Lc >> 1) | (next_lo << 31) | (beyond >> 1);  // land at x+1
+            const uint32_t Ll = (Lc << 1) | prev_hi;                         // land at x-1
+            const uint32_t coast_bits = Lc & ~(Ll & Lr & Lu & Ld);
+            if (bits) bits[y * words + w] = coast_bits;
+            land += __popc(Lc);
+            coast += __popc(coast_bits);
+            if (mask8) {
+                const int64_t nbit = valid >= 32 ? 32 : valid;
+                for (int b = 0; b < nbit; ++b) mask8[y * R + w * 32 + b] = (coast_bits >> b) & 1u;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        land += __shfl_xor_sync(0xffffffffu, land, o);
+        coast += __shfl_xor_sync(0xffffffffu, coast, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&counts[0], land);
+        atomicAdd(&counts[1], coast);
+    }
+}
+
+__global__ void pack_mask_kernel(const uint8_t* __restrict__ m, int64_t R, uint32_t* __restrict__ bits,
+                                 unsigned long long* __restrict__ counts) {
+    const int64_t words = (R + 31) / 32;
+    unsigned long long pix = 0;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < R * words;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t y = t / words, w = t - y * words;
+        uint32_t v = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int64_t x = w * 32 + b;
+            if (x < R && m[y * R + x]) v |= 1u << b;
+        }
+        bits[t] = v;
+        pix += __popc(v);
+    }
+    atomicAdd(&counts[1], pix);
+}
+
+// Occupied boxes of side eps (partial far-edge boxes count, analysis.hpp:284).
+__global__ void boxcount_kernel(const uint32_t* __restrict__ bits, int64_t R, const int32_t* sizes,
+                                int n_sizes, unsigned long long* __restrict__ out) {
+    const int s = blockIdx.y;
+    if (s >= n_sizes) return;
+    const int64_t eps = sizes[s];
+    const int64_t words = (R + 31) / 32;
+    const int64_t bpa = (R + eps - 1) / eps;
+    unsigned long long occ = 0;
+    for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < bpa * bpa;
+         b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t by = b / bpa, bx = b - by * bpa;
+        const int64_t x0 = bx * eps, x1 = min(R, x0 + eps);
+        const int64_t y0 = by * eps, y1 = min(R, y0 + eps);
+        const int64_t wa = x0 >> 5, wb = (x1 - 1) >> 5;
+        bool hit = false;
+        for (int64_t y = y0; y < y1 && !hit; ++y) {
+            const uint32_t* row = bits + y * words;
+            for (int64_t w = wa; w <= wb; ++w) {
+                uint32_t m = 0xffffffffu;
+                if (w == wa) m &= 0xffffffffu << (x0 & 31);
+                if (w == wb) {
+                    const int hi = static_cast<int>((x1 - 1) & 31);
+                    m &= hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u);
+                }
+                if (row[w] & m) {
+                    hit = true;
+                    break;
+                }
+            }
+        }
+        occ += hit ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
+    if ((threadIdx.x & 31) == 0 && occ) atomicAdd(&out[s], occ);
+}
+
+// ---- variogram ----------------------------------------------------------------
+constexpr int kMaxLags = 32;
+
+__global__ void variogram_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld,
+                                 const int32_t* __restrict__ lags, int n_lags,
+                                 double* __restrict__ sums) {
+    // blockIdx.y = 2*lag + axis
+    const int q = blockIdx.y;
+    const int li = q >> 1, axis = q & 1;
+    const int64_t h = lags[li];
+    const int64_t nx = axis == 0 ? W - h : W;
+    const int64_t ny = axis == 0 ? H : H - h;
+    double acc = 0.0;
+    if (nx > 0 && ny > 0) {
+        const int64_t off = axis == 0 ? h : h * ld;
+        for (int64_t y = blockIdx.x; y < ny; y += gridDim.x) {
+            const float* row = z + y * ld;
+            for (int64_t x = threadIdx.x; x < nx; x += blockDim.x) {
+                // difference of two fp32 values is exact in fp64
+                const double d = static_cast<double>(row[x + off]) - static_cast<double>(row[x]);
+                acc = fma(d, d, acc);
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double part[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        acc = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) atomicAdd(&sums[q], acc);
+    }
+}
+
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, n, s); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+}  // namespace
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" {
+
+int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* stream) {
+    if (!dev_map || !out_median || n == 0)
+        return set_error(TG_EVALIDATION, "coastline_mask: empty heightmap");
+    if (int st = check_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Scratch scr(s);
+    cudaError_t e = scr.alloc(sizeof(SelectState) + kBins * sizeof(unsigned long long));
+    if (e != cudaSuccess) return set_cuda_error(e, "median alloc");
+    SelectState* state = static_cast<SelectState*>(scr.p);
+    unsigned long long* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);
+    SelectState init{0u, 0u, n / 2};  // analysis.hpp:247 (upper median)
+    e = cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned long long), s);
+    const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
+    for (int p = 0; p < 3 && e == cudaSuccess; ++p) {
+        radix_hist<<<148 * 4, 512, 0, s>>>(dev_map, n, state, shifts[p], widths[p], hist);
+        radix_pick<<<1, 32, 0, s>>>(state, hist, shifts[p], widths[p]);
+        e = cudaGetLastError();
+    }
+    SelectState res{};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&res, state, sizeof(res), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_cuda_error(e, "median");
+    const uint32_t k = res.prefix;
+    const uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    std::memcpy(out_median, &b, 4);
+    return TG_OK;
+}
+
+static int coast_common(const float* dev_map, int64_t R, double sea, uint32_t* bits, uint8_t* mask8,
+                        unsigned long long* counts, cudaStream_t s) {
+    const int64_t segs = ((R + 31) / 32 + 31) / 32;
+    const int64_t warps = R * segs;
+    const int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, 148 * 16);
+    // land test h >= sea with the fp32 map widened exactly: for a double sea
+    // level, h >= sea  <=>  h >= the smallest float >= sea.
+    float seaf = static_cast<float>(sea);
+    if (static_cast<double>(seaf) < sea) seaf = nextafterf(seaf, INFINITY);
+    coast_bits_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(dev_map, R, seaf, bits, mask8, counts);
+    return cudaGetLastError() == cudaSuccess ? TG_OK : set_error(TG_EDEVICE, "coastline kernel launch");
+}
+
+int tg_coastline_mask(const float* dev_map, int64_t resolution, double sea_level, uint8_t* dev_mask,
+                      int64_t* out_land_count, void* stream) {
+    if (resolution < 2) return set_error(TG_EVALIDATION, "coastline_mask: resolution must be at least 2");
+    if (!dev_map || !dev_mask) return set_error(TG_EVALIDATION, "coastline_mask: null pointer");
+    if (int st = check_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Scratch scr(s);
+    cudaError_t e = scr.alloc(2 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return set_cuda_error(e, "coastline alloc");
+    auto* counts = static_cast<unsigned long long*>(scr.p);
+    e = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return set_cuda_error(e, "coastline memset");
+    if (int st = coast_common(dev_map, resolution, sea_level, nullptr, dev_mask, counts, s)) return st;
+    unsigned long long h[2];
+    e = cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_cuda_error(e, "coastline");
+    if (out_land_count) *out_land_count = static_cast<int64_t>(h[0]);
+    const unsigned long long total = static_cast<unsigned long long>(resolution) * resolution;
+    if (h[0] == 0 || h[0] == total)  // analysis.hpp:237-238
+        return set_error(TG_EVALIDATION, "coastline_mask: map is entirely land or entirely water");
+    return TG_OK;
+}
+
+static int check_sizes(int64_t R, const int32_t* sizes, int32_t n) {
+    if (n < 3 || n > 64) return set_error(TG_EVALIDATION, "box_count: need at least 3 box sizes to fit");
+    for (int i = 0; i < n; ++i) {  // analysis.hpp:272-278
+        if (sizes[i] < 1 || sizes[i] > R)
+            return set_error(TG_EVALIDATION, "box_count: box sizes must lie in [1, resolution]");
+        if (i > 0 && sizes[i] <= sizes[i - 1])
+            return set_error(TG_EVALIDATION, "box_count: box sizes must be strictly increasing");
+    }
+    return TG_OK;
+}
+
+static int boxcount_from_bits(const uint32_t* bits, int64_t R, const int32_t* sizes, int32_t n,
+                              unsigned long long* dcounts, int32_t* dsizes, int64_t* out_counts,
+                              cudaStream_t s) {
+    cudaError_t e = cudaMemcpyAsync(dsizes, sizes, n * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "boxcount sizes");
+    dim3 grid(148 * 2, static_cast<unsigned>(n));
+    boxcount_kernel<<<grid, 256, 0, s>>>(bits, R, dsizes, n, dcounts);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "boxcount launch");
+    return TG_OK;
+}
+
+int tg_coastline_boxcount(const float* dev_map, int64_t resolution, double sea_level, const int32_t* sizes,
+                          int32_t n_sizes, int64_t* out_counts, int64_t* out_coast_pixels,
+                          int64_t* out_land_count, void* stream) {
+    if (resolution < 2) return set_error(TG_EVALIDATION, "coastline_mask: resolution must be at least 2");
+    if (!dev_map || !sizes || !out_counts) return set_error(TG_EVALIDATION, "coastline_boxcount: null pointer");
+    if (int st = check_sizes(resolution, sizes, n_sizes)) return st;
+    if (int st = check_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t words = (resolution + 31) / 32;
+    const size_t bits_bytes = static_cast<size_t>(resolution * words) * 4;
+    Scratch scr(s);
+    const size_t hdr = 2 * 8 + 64 * 8 + 64 * 4;
+    cudaError_t e = scr.alloc(hdr + bits_bytes);
+    if (e != cudaSuccess) return set_cuda_error(e, "coastline_boxcount alloc");
+    auto* counts = static_cast<unsigned long long*>(scr.p);
+    auto* bcounts = counts + 2;
+    auto* dsizes = reinterpret_cast<int32_t*>(bcounts + 64);
+    auto* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(scr.p) + hdr);
+    e = cudaMemsetAsync(scr.p, 0, 2 * 8 + 64 * 8, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "coastline_boxcount memset");
+    if (int st = coast_common(dev_map, resolution, sea_level, bits, nullptr, counts, s)) return st;
+    if (int st = boxcount_from_bits(bits, resolution, sizes, n_sizes, bcounts, dsizes, out_counts, s)) return st;
+    unsigned long long h[2 + 64];
+    e = cudaMemcpyAsync(h, counts, (2 + n_sizes) * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_cuda_error(e, "coastline_boxcount");
+    if (out_land_count) *out_land_count = static_cast<int64_t>(h[0]);
+    if (out_coast_pixels) *out_coast_pixels = static_cast<int64_t>(h[1]);
+    for (int i = 0; i < n_sizes; ++i) out_counts[i] = static_cast<int64_t>(h[2 + i]);
+    const unsigned long long total = static_cast<unsigned long long>(resolution) * resolution;
+    if (h[0] == 0 || h[0] == total)
+        return set_error(TG_EVALIDATION, "coastline_mask: map is entirely land or entirely water");
+    if (h[1] == 0) return set_error(TG_EVALIDATION, "box_count: empty coastline mask");
+    return TG_OK;
+}
+
+int tg_boxcount_mask(const uint8_t* dev_mask, int64_t resolution, const int32_t* sizes, int32_t n_sizes,
+                     int64_t* out_counts, void* stream) {
+    if (resolution < 2) return set_error(TG_EVALIDATION, "box_count: invalid mask resolution");
+    if (!dev_mask || !sizes || !out_counts) return set_error(TG_EVALIDATION, "box_count: null pointer");
+    if (int st = check_sizes(resolution, sizes, n_sizes)) return st;
+    if (int st = check_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t words = (resolution + 31) / 32;
+    const size_t bits_bytes = static_cast<size_t>(resolution * words) * 4;
+    Scratch scr(s);
+    const size_t hdr = 2 * 8 + 64 * 8 + 64 * 4;
+    cudaError_t e = scr.alloc(hdr + bits_bytes);
+    if (e != cudaSuccess) return set_cuda_error(e, "box_count alloc");
+    auto* counts = static_cast<unsigned long long*>(scr.p);
+    auto* bcounts = counts + 2;
+    auto* dsizes = reinterpret_cast<int32_t*>(bcounts + 64);
+    auto* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(scr.p) + hdr);
+    e = cudaMemsetAsync(scr.p, 0, 2 * 8 + 64 * 8, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "box_count memset");
+    pack_mask_kernel<<<148 * 8, 256, 0, s>>>(dev_mask, resolution, bits, counts);
+    if (int st = boxcount_from_bits(bits, resolution, sizes, n_sizes, bcounts, dsizes, out_counts, s)) return st;
+    unsigned long long h[2 + 64];
+    e = cudaMemcpyAsync(h, counts, (2 + n_sizes) * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_cuda_error(e, "box_count");
+    for (int i = 0; i < n_sizes; ++i) out_counts[i] = static_cast<int64_t>(h[2 + i]);
+    if (h[1] == 0) return set_error(TG_EVALIDATION, "box_count: empty coastline mask");
+    return TG_OK;
+}
+
+int tg_variogram_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld, const int32_t* lags,
+                     int32_t n_lags, double* out_sum_sq, int64_t* out_pairs, void* stream) {
+    if (!dev_map || !lags || !out_sum_sq || !out_pairs) return set_error(TG_EVALIDATION, "variogram: null pointer");
+    if (width < 1 || height < 1 || ld < width) return set_error(TG_EVALIDATION, "variogram: bad window");
+    if (n_lags < 1 || n_lags > kMaxLags) return set_error(TG_EVALIDATION, "variogram: 1..32 lags");
+    for (int i = 0; i < n_lags; ++i)
+        if (lags[i] < 1) return set_error(TG_EVALIDATION, "variogram: lags must be >= 1");
+    if (int st = check_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Scratch scr(s);
+    cudaError_t e = scr.alloc(2 * kMaxLags * sizeof(double) + kMaxLags * sizeof(int32_t));
+    if (e != cudaSuccess) return set_cuda_error(e, "variogram alloc");
+    auto* sums = static_cast<double*>(scr.p);
+    auto* dl = reinterpret_cast<int32_t*>(sums + 2 * kMaxLags);
+    e = cudaMemsetAsync(sums, 0, 2 * kMaxLags * sizeof(double), s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dl, lags, n_lags * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "variogram setup");
+    dim3 grid(148 * 2, static_cast<unsigned>(2 * n_lags));
+    variogram_kernel<<<grid, 256, 0, s>>>(dev_map, width, height, ld, dl, n_lags, sums);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_sum_sq, sums, 2 * n_lags * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_cuda_error(e, "variogram");
+    for (int i = 0; i < n_lags; ++i) {
+        const int64_t h = lags[i];
+        out_pairs[2 * i] = h < width ? (width - h) * height : 0;
+        out_pairs[2 * i + 1] = h < height ? width * (height - h) : 0;
+    }
+    return TG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,428 @@
+// capi.cu — C-ABI entry points (include/polyterrain_b200.h), validation and
+// the per-call octave planner.
+//
+// Host logic restated from terrain/fbm.hpp:
+//   FbmConfig::validate        fbm.hpp:71-88   -> tg_fbm_validate
+//   detail::octave_spec        fbm.hpp:151-168 -> tg_fbm_octave_spec / plan()
+//   window checks              fbm.hpp:546-558 -> tg_fbm_validate_window
+//   generate_into_with_source  fbm.hpp:541-628 -> tg_fbm_generate_*_f32
+// Errors map onto terrain/errors.hpp through the tg_status codes.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/polyterrain_b200.h"
+#include "fbm_params.h"
+#include "lattice.cuh"
+
+namespace tg {
+cudaError_t fbm2d_launch(int kind, int order, const FbmArgs& a, float* out, cudaStream_t st);
+int fbm2d_tile_h();
+cudaError_t fbm3d_launch(int order, const Fbm3Args& a, float* out, cudaStream_t st);
+void fbm3d_tile(int* tx, int* ty, int* tz);
+cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uint64_t lane,
+                           void* out, cudaStream_t st);
+cudaError_t widen_launch(const float* in, double* out, uint64_t n, cudaStream_t st);
+}  // namespace tg
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(TG_EDEVICE, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TG_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+int64_t floor_div(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int order_of(const tg_fbm_config* c) {
+    if (c->smoothstep) return c->smoothstep;
+    return c->method == TG_METHOD_PERLIN5 ? 5 : 3;  // fbm.hpp:66-69
+}
+
+int kind_of(const tg_fbm_config* c) {
+    switch (c->method) {
+        case TG_METHOD_ZG_PAPER: return tg::kZgPaper;
+        case TG_METHOD_ZG_SEPARABLE: return tg::kZgSeparable;
+        case TG_METHOD_GENERIC: return tg::kGeneric;
+        default: return tg::kPerlin;
+    }
+}
+
+void octave_spec(const tg_fbm_config* c, int octave, tg_octave_spec* os) {
+    os->freq = static_cast<double>(c->base_frequency);
+    os->amp = c->base_amplitude;
+    for (int k = 0; k < octave; ++k) {  // repeated multiplication, fbm.hpp:155-158
+        os->freq *= c->frequency_ratio;
+        os->amp *= c->persistence;
+    }
+    os->fast = 0;
+    os->cells = 0;
+    os->ppc = 0;
+    const double rounded = std::floor(os->freq);
+    if (rounded == os->freq && rounded >= 1.0 && rounded <= static_cast<double>(c->resolution) &&
+        c->resolution % static_cast<long long>(rounded) == 0) {
+        os->fast = 1;
+        os->cells = static_cast<int64_t>(rounded);
+        os->ppc = static_cast<int32_t>(c->resolution / os->cells);
+    }
+}
+
+// Fill the per-octave device plan for windows whose global coordinates stay
+// within |g| <= gmax.
+void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out) {
+    const double R = static_cast<double>(c->resolution);
+    const double w = c->has_gradient_weight ? c->gradient_weight : c->base_amplitude / 100.0;
+    for (int o = 0; o < c->octaves; ++o) {
+        tg_octave_spec os;
+        octave_spec(c, o, &os);
+        tg::OctDev& d = out[o];
+        std::memset(&d, 0, sizeof(d));
+        d.oct_key = static_cast<uint64_t>(static_cast<uint32_t>(o)) * tg::kOctMul;
+        d.freq = os.freq;
+        d.amp = static_cast<float>(os.amp);
+        d.w = static_cast<float>(w);
+        d.shift = -1;
+        if (os.fast) {
+            d.cls = tg::kClsFast;
+            d.ppc = os.ppc;
+            d.inv_ppc = 1.0f / static_cast<float>(os.ppc);
+            if (is_pow2(os.ppc)) {
+                int s = 0;
+                while ((1LL << s) < os.ppc) ++s;
+                d.shift = s;
+            }
+            continue;
+        }
+        d.cls = tg::kClsGeneral;
+        // Exact lattice-point sampling: R = 2^n and freq = k*R with k even make
+        // ((g + 0.5)/R)*freq = g*k + k/2 exactly in fp64 (no rounding while
+        // |g*k| < 2^52), so render_general sees cx = cy = 0 (fbm.hpp:468-489).
+        if (is_pow2(c->resolution)) {
+            const double kd = os.freq / R;
+            if (kd >= 2.0 && kd < 9.0e15 && std::floor(kd) == kd && kd * R == os.freq) {
+                const int64_t k = static_cast<int64_t>(kd);
+                const double bound = (static_cast<double>(gmax) + 1.0) * kd + kd;
+                if ((k & 1) == 0 && bound < 4.0e15) {
+                    d.cls = tg::kClsSubInt;
+                    d.k = k;
+                }
+            }
+        }
+    }
+}
+
+int validate_cfg(const tg_fbm_config* c) {
+    if (!c) return fail(TG_EVALIDATION, "fbm config: null");
+    if (c->octaves < 1 || c->octaves > TG_MAX_OCTAVES)
+        return fail(TG_EVALIDATION, "fbm config: octaves must be in [1, 32]");
+    if (c->resolution < 1 || c->resolution > TG_MAX_RESOLUTION)
+        return fail(TG_EVALIDATION, "fbm config: resolution must be in [1, 4194304]");
+    if (c->base_frequency < 1 || c->base_frequency > TG_MAX_RESOLUTION)
+        return fail(TG_EVALIDATION, "fbm config: base_frequency must be in [1, 4194304]");
+    if (!(c->frequency_ratio > 1.0) || !std::isfinite(c->frequency_ratio))
+        return fail(TG_EVALIDATION, "fbm config: frequency_ratio must be > 1");
+    if (!(c->persistence > 0.0 && c->persistence <= 1.0))
+        return fail(TG_EVALIDATION, "fbm config: persistence must lie in (0, 1]");
+    if (!(c->base_amplitude > 0.0) || !std::isfinite(c->base_amplitude))
+        return fail(TG_EVALIDATION, "fbm config: base_amplitude must be positive");
+    if (c->has_gradient_weight && (!(c->gradient_weight >= 0.0) || !std::isfinite(c->gradient_weight)))
+        return fail(TG_EVALIDATION, "fbm config: gradient_weight must be non-negative");
+    if (c->threads < 0 || c->threads > 256)
+        return fail(TG_EVALIDATION, "fbm config: threads must be in [0, 256]");
+    if (c->method < TG_METHOD_ZG_PAPER || c->method > TG_METHOD_PERLIN5)
+        return fail(TG_EVALIDATION, "fbm config: unknown method");
+    if (c->smoothstep != 0 && c->smoothstep != 3 && c->smoothstep != 5)
+        return fail(TG_EVALIDATION, "fbm config: smoothstep must be 0, 3 or 5");
+    return TG_OK;
+}
+
+int validate_window(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width,
+                    int64_t height) {
+    if (width < 1 || width > TG_MAX_EXTENT || height < 1 || height > TG_MAX_EXTENT)
+        return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
+    const int64_t origin[2] = {ox, oy};
+    for (const int64_t o : origin) {  // fbm.hpp:551-558
+        if (o < -(1LL << 40) || o > (1LL << 40))
+            return fail(TG_EVALIDATION, "generate: origin out of supported range");
+        const int64_t prod = o * c->base_frequency;
+        if (((prod % c->resolution) + c->resolution) % c->resolution != 0)
+            return fail(TG_EVALIDATION, "generate: origin must be aligned to octave-0 cell boundaries");
+    }
+    return TG_OK;
+}
+
+int device_ready() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(TG_EDEVICE, "no CUDA device: the B200 path has no CPU fallback");
+    }
+    return TG_OK;
+}
+
+int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, int64_t height,
+               int64_t ld, tg::FbmArgs* a) {
+    std::memset(a, 0, sizeof(*a));
+    a->ox = ox;
+    a->oy = oy;
+    a->width = width;
+    a->height = height;
+    a->ld = ld;
+    a->map_stride = ld * height;
+    a->tile_x0 = floor_div(ox, 128) * 128;
+    a->tile_y0 = floor_div(oy, tg::fbm2d_tile_h()) * tg::fbm2d_tile_h();
+    a->R = static_cast<double>(c->resolution);
+    a->octaves = c->octaves;
+    a->zero = c->zero_lattice ? 1 : 0;
+    a->n_maps = 1;
+    a->seed_key[0] = c->seed * tg::kSeedMul;
+    int64_t gmax = 0;
+    const int64_t cand[4] = {ox - 256, ox + width + 256, oy - 256, oy + height + 256};
+    for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
+    plan_octaves(c, gmax, a->oct);
+    return TG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tg_abi_version(void) { return TG_ABI_VERSION; }
+
+const char* tg_last_error(void) { return g_err.c_str(); }
+
+int tg_fbm_validate(const tg_fbm_config* cfg) { return validate_cfg(cfg); }
+
+int tg_fbm_octave_spec(const tg_fbm_config* cfg, int32_t octave, tg_octave_spec* out) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (!out || octave < 0 || octave >= cfg->octaves)
+        return fail(TG_EVALIDATION, "octave_spec: octave out of range");
+    octave_spec(cfg, octave, out);
+    return TG_OK;
+}
+
+int tg_fbm_validate_window(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
+                           int64_t height) {
+    if (int st = validate_cfg(cfg)) return st;
+    return validate_window(cfg, ox, oy, width, height);
+}
+
+int tg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int tg_fbm_generate_rect_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
+                             int64_t height, float* dev_out, int64_t ld, void* stream) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (int st = validate_window(cfg, ox, oy, width, height)) return st;
+    if (!dev_out) return fail(TG_EVALIDATION, "generate: null output");
+    if (ld < width) return fail(TG_EVALIDATION, "generate: row pitch smaller than width");
+    if (int st = device_ready()) return st;
+    tg::FbmArgs a;
+    build_args(cfg, ox, oy, width, height, ld, &a);
+    TG_CUDA(tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, dev_out,
+                             static_cast<cudaStream_t>(stream)));
+    return TG_OK;
+}
+
+int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                        float* dev_out, uint64_t n_out, void* stream) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (extent < 1 || extent > TG_MAX_EXTENT)
+        return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
+    if (n_out != static_cast<uint64_t>(extent) * static_cast<uint64_t>(extent))
+        return fail(TG_EVALIDATION, "generate: output buffer size mismatch");  // fbm.hpp:549
+    return tg_fbm_generate_rect_f32(cfg, ox, oy, extent, extent, dev_out, extent, stream);
+}
+
+int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, int32_t n_seeds,
+                              int64_t ox, int64_t oy, int64_t width, int64_t height,
+                              float* dev_out, void* stream) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (int st = validate_window(cfg, ox, oy, width, height)) return st;
+    if (!seeds || n_seeds < 1 || !dev_out) return fail(TG_EVALIDATION, "batch: bad arguments");
+    if (int st = device_ready()) return st;
+    tg::FbmArgs a;
+    build_args(cfg, ox, oy, width, height, width, &a);
+    for (int32_t b0 = 0; b0 < n_seeds; b0 += tg::kMaxBatch) {
+        const int nb = std::min<int32_t>(tg::kMaxBatch, n_seeds - b0);
+        a.n_maps = nb;
+        for (int i = 0; i < nb; ++i) a.seed_key[i] = seeds[b0 + i] * tg::kSeedMul;
+        TG_CUDA(tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a,
+                                 dev_out + static_cast<int64_t>(b0) * width * height,
+                                 static_cast<cudaStream_t>(stream)));
+    }
+    return TG_OK;
+}
+
+// Host-buffer forms: the drop-in for generate_into(cfg, origin, extent,
+// std::span<double>) (fbm.hpp:630-634).  Device work is fp32; the result is
+// produced in row bands so the next band's generation overlaps the previous
+// band's device->host copy.
+static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                         void* host_out, uint64_t n_out, bool f64) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (extent < 1 || extent > TG_MAX_EXTENT)
+        return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
+    if (n_out != static_cast<uint64_t>(extent) * static_cast<uint64_t>(extent))
+        return fail(TG_EVALIDATION, "generate: output buffer size mismatch");
+    if (!host_out) return fail(TG_EVALIDATION, "generate: null output");
+    if (int st = validate_window(cfg, ox, oy, extent, extent)) return st;
+    if (int st = device_ready()) return st;
+
+    const int64_t th = tg::fbm2d_tile_h();
+    // Bands of whole tile rows, ~8 MiB of fp32 each.
+    int64_t band = std::max<int64_t>(th, (static_cast<int64_t>(2) << 20) / extent / th * th);
+    band = std::min<int64_t>(band, extent);
+    const size_t elem = f64 ? sizeof(double) : sizeof(float);
+    cudaStream_t st[2];
+    TG_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
+    TG_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+    float* dev32[2] = {nullptr, nullptr};
+    double* dev64[2] = {nullptr, nullptr};
+    const size_t band_elems = static_cast<size_t>(band) * static_cast<size_t>(extent);
+    int rc = TG_OK;
+    for (int i = 0; i < 2 && rc == TG_OK; ++i) {
+        if (cudaMallocAsync(reinterpret_cast<void**>(&dev32[i]), band_elems * sizeof(float), st[i]) != cudaSuccess)
+            rc = fail(TG_EDEVICE, "generate: device allocation failed");
+        if (f64 && rc == TG_OK &&
+            cudaMallocAsync(reinterpret_cast<void**>(&dev64[i]), band_elems * sizeof(double), st[i]) != cudaSuccess)
+            rc = fail(TG_EDEVICE, "generate: device allocation failed");
+    }
+    if (rc == TG_OK) {
+        tg::FbmArgs a;
+        int bi = 0;
+        for (int64_t y0 = 0; y0 < extent && rc == TG_OK; y0 += band, bi ^= 1) {
+            const int64_t h = std::min<int64_t>(band, extent - y0);
+            build_args(cfg, ox, oy + y0, extent, h, extent, &a);
+            cudaError_t e = tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, dev32[bi], st[bi]);
+            const void* src = dev32[bi];
+            if (e == cudaSuccess && f64) {
+                e = tg::widen_launch(dev32[bi], dev64[bi], static_cast<uint64_t>(h * extent), st[bi]);
+                src = dev64[bi];
+            }
+            char* dst = static_cast<char*>(host_out) + static_cast<size_t>(y0) * extent * elem;
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(dst, src, static_cast<size_t>(h) * extent * elem,
+                                    cudaMemcpyDeviceToHost, st[bi]);
+            if (e != cudaSuccess) rc = cuda_fail(e, "generate_host");
+        }
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (dev32[i]) cudaFreeAsync(dev32[i], st[i]);
+        if (dev64[i]) cudaFreeAsync(dev64[i], st[i]);
+        cudaError_t e = cudaStreamSynchronize(st[i]);
+        if (e != cudaSuccess && rc == TG_OK) rc = cuda_fail(e, "generate_host sync");
+        cudaStreamDestroy(st[i]);
+    }
+    return rc;
+}
+
+int tg_fbm_generate_f64_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                             double* host_out, uint64_t n_out) {
+    return generate_host(cfg, ox, oy, extent, host_out, n_out, true);
+}
+
+int tg_fbm_generate_f32_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
+                             float* host_out, uint64_t n_out) {
+    return generate_host(cfg, ox, oy, extent, host_out, n_out, false);
+}
+
+int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t oz,
+                          int64_t nx, int64_t ny, int64_t nz, float* dev_out, void* stream) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (cfg->method != TG_METHOD_ZG_SEPARABLE)
+        return fail(TG_EVALIDATION, "fbm3d: only the separable zero-gradient cell is defined in 3D");
+    if (nx < 1 || ny < 1 || nz < 1 || nx > TG_MAX_EXTENT || ny > TG_MAX_EXTENT || nz > TG_MAX_EXTENT)
+        return fail(TG_EVALIDATION, "fbm3d: extent out of range");
+    if (int st = validate_window(cfg, ox, oy, 1, 1)) return st;
+    if (int st = validate_window(cfg, oz, 0, 1, 1)) return st;
+    if (!dev_out) return fail(TG_EVALIDATION, "fbm3d: null output");
+    if (int st = device_ready()) return st;
+    tg::Fbm3Args a;
+    std::memset(&a, 0, sizeof(a));
+    int tx, ty, tz;
+    tg::fbm3d_tile(&tx, &ty, &tz);
+    a.ox = ox;
+    a.oy = oy;
+    a.oz = oz;
+    a.nx = nx;
+    a.ny = ny;
+    a.nz = nz;
+    a.tile_x0 = floor_div(ox, tx) * tx;
+    a.tile_y0 = floor_div(oy, ty) * ty;
+    a.tile_z0 = floor_div(oz, tz) * tz;
+    a.R = static_cast<double>(cfg->resolution);
+    a.octaves = cfg->octaves;
+    a.zero = cfg->zero_lattice ? 1 : 0;
+    a.seed_key = cfg->seed * tg::kSeedMul;
+    int64_t gmax = 0;
+    const int64_t cand[6] = {ox - 64, ox + nx + 64, oy - 64, oy + ny + 64, oz - 64, oz + nz + 64};
+    for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
+    plan_octaves(cfg, gmax, a.oct);
+    TG_CUDA(tg::fbm3d_launch(order_of(cfg), a, dev_out, static_cast<cudaStream_t>(stream)));
+    return TG_OK;
+}
+
+int tg_lattice_hash(const tg_lattice_key* dev_keys, uint64_t n, uint64_t lane, uint64_t* dev_out,
+                    void* stream) {
+    if (n == 0) return TG_OK;
+    if (!dev_keys || !dev_out) return fail(TG_EVALIDATION, "lattice_hash: null pointer");
+    if (int st = device_ready()) return st;
+    TG_CUDA(tg::lattice_launch(0, dev_keys, n, lane, dev_out, static_cast<cudaStream_t>(stream)));
+    return TG_OK;
+}
+
+int tg_lattice_height_f32(const tg_lattice_key* dev_keys, uint64_t n, float* dev_out,
+                          void* stream) {
+    if (n == 0) return TG_OK;
+    if (!dev_keys || !dev_out) return fail(TG_EVALIDATION, "lattice_height: null pointer");
+    if (int st = device_ready()) return st;
+    TG_CUDA(tg::lattice_launch(1, dev_keys, n, 0, dev_out, static_cast<cudaStream_t>(stream)));
+    return TG_OK;
+}
+
+int tg_lattice_unit_gradient_f32(const tg_lattice_key* dev_keys, uint64_t n, float* dev_out,
+                                 void* stream) {
+    if (n == 0) return TG_OK;
+    if (!dev_keys || !dev_out) return fail(TG_EVALIDATION, "lattice_unit_gradient: null pointer");
+    if (int st = device_ready()) return st;
+    TG_CUDA(tg::lattice_launch(2, dev_keys, n, 0, dev_out, static_cast<cudaStream_t>(stream)));
+    return TG_OK;
+}
+
+}  // extern "C"
+
+// Error helpers for the other translation units.
+namespace tg {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+int check_device() { return device_ready(); }
+}  // namespace tg

@@ -1,0 +1,200 @@
+// kernels.cu — small device kernels behind the C-ABI: lattice probes
+// (lattice.hpp parity), fp32->fp64 widening for the drop-in span<double>,
+// min/max + rescale (normalize_map, fbm.hpp:638-656) and the FFMA-chain
+// peak used as the FP32 roofline denominator.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/polyterrain_b200.h"
+#include "lattice.cuh"
+
+namespace tg {
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t e, const char* where);
+int check_device();
+
+__global__ void lattice_kernel(int what, const tg_lattice_key* __restrict__ keys, uint64_t n,
+                               uint64_t lane, void* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const tg_lattice_key k = keys[i];
+        const uint64_t base = k.seed * kSeedMul + static_cast<uint64_t>(k.octave) * kOctMul;
+        if (what == 0) {
+            static_cast<uint64_t*>(out)[i] = mix64(pack_xy(base, k.ix, k.iy) ^ lane);
+        } else if (what == 1) {
+            static_cast<float*>(out)[i] = corner_height(base, k.ix, k.iy);
+        } else {
+            float c, s;
+            corner_unit_gradient(base, k.ix, k.iy, &c, &s);
+            static_cast<float*>(out)[2 * i] = c;
+            static_cast<float*>(out)[2 * i + 1] = s;
+        }
+    }
+}
+
+cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uint64_t lane,
+                           void* out, cudaStream_t st) {
+    const uint64_t blocks = (n + 255) / 256;
+    lattice_kernel<<<static_cast<unsigned>(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, st>>>(
+        what, keys, n, lane, out);
+    return cudaGetLastError();
+}
+
+__global__ void widen_kernel(const float* __restrict__ in, double* __restrict__ out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<double>(in[i]);
+}
+
+cudaError_t widen_launch(const float* in, double* out, uint64_t n, cudaStream_t st) {
+    widen_kernel<<<148 * 8, 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+// Order-preserving float <-> uint32 key (for min/max atomics and radix select).
+__device__ __forceinline__ uint32_t fkey(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__global__ void minmax_kernel(const float* __restrict__ x, uint64_t n, uint32_t* __restrict__ mm) {
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    const uint64_t n4 = n / 4;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (aligned) {
+        for (uint64_t i = i0; i < n4; i += stride) {
+            const float4 v = x4[i];
+            const uint32_t a = fkey(v.x), b = fkey(v.y), c = fkey(v.z), d = fkey(v.w);
+            lo = min(lo, min(min(a, b), min(c, d)));
+            hi = max(hi, max(max(a, b), max(c, d)));
+        }
+        for (uint64_t i = n4 * 4 + i0; i < n; i += stride) {
+            const uint32_t a = fkey(x[i]);
+            lo = min(lo, a);
+            hi = max(hi, a);
+        }
+    } else {
+        for (uint64_t i = i0; i < n; i += stride) {
+            const uint32_t a = fkey(x[i]);
+            lo = min(lo, a);
+            hi = max(hi, a);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
+__global__ void rescale_kernel(float* __restrict__ x, uint64_t n, double lo, double span) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        x[i] = static_cast<float>(-1.0 + 2.0 * (static_cast<double>(x[i]) - lo) / span);  // fbm.hpp:653
+}
+
+// Eight independent FFMA chains per thread: issue-bound FP32 peak.
+__global__ void ffma_kernel(float* out, int iters) {
+    float a0 = threadIdx.x * 1e-7f, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+    float a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+    const float m = 0.9999999f, c = 1e-7f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fmaf(a0, m, c); a1 = fmaf(a1, m, c); a2 = fmaf(a2, m, c); a3 = fmaf(a3, m, c);
+            a4 = fmaf(a4, m, c); a5 = fmaf(a5, m, c); a6 = fmaf(a6, m, c); a7 = fmaf(a7, m, c);
+        }
+    }
+    const float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 123.456f) out[0] = s;
+}
+
+}  // namespace tg
+
+extern "C" {
+
+int tg_minmax_f32(const float* dev_map, uint64_t n, double* out_min, double* out_max,
+                  void* stream) {
+    if (!dev_map || !out_min || !out_max || n == 0)
+        return tg::set_error(TG_EVALIDATION, "minmax: empty or null input");
+    if (int st = tg::check_device()) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t* mm = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&mm), 2 * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "minmax alloc");
+    const uint32_t init[2] = {0xffffffffu, 0u};
+    uint32_t res[2];
+    e = cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        tg::minmax_kernel<<<148 * 4, 256, 0, s>>>(dev_map, n, mm);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(res, mm, sizeof(res), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(mm, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "minmax");
+    const auto unkey = [](uint32_t k) {
+        const uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+        float f;
+        std::memcpy(&f, &b, 4);
+        return static_cast<double>(f);
+    };
+    *out_min = unkey(res[0]);
+    *out_max = unkey(res[1]);
+    return TG_OK;
+}
+
+int tg_rescale_f32(float* dev_map, uint64_t n, double lo, double hi, void* stream) {
+    if (!dev_map) return tg::set_error(TG_EVALIDATION, "rescale: null input");
+    if (!(hi > lo)) return tg::set_error(TG_EVALIDATION, "rescale: empty range");
+    if (n == 0) return TG_OK;
+    if (int st = tg::check_device()) return st;
+    tg::rescale_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(dev_map, n, lo,
+                                                                                 hi - lo);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "rescale");
+    return TG_OK;
+}
+
+int tg_measure_ffma_peak(double* out_tflops, double* out_ms) {
+    if (int st = tg::check_device()) return st;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    float* sink = nullptr;
+    cudaError_t e = cudaMalloc(&sink, sizeof(float));
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "ffma alloc");
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    tg::ffma_kernel<<<blocks, threads>>>(sink, 64);  // warm-up / clock ramp
+    tg::ffma_kernel<<<blocks, threads>>>(sink, iters);
+    cudaEventRecord(a);
+    tg::ffma_kernel<<<blocks, threads>>>(sink, iters);
+    cudaEventRecord(b);
+    e = cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "ffma");
+    const double flops = 2.0 * 8.0 * 16.0 * iters * static_cast<double>(blocks) * threads;
+    *out_tflops = flops / (ms * 1e-3) / 1e12;
+    if (out_ms) *out_ms = ms;
+    return TG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// lattice.cuh — seeded corner data on the device (terrain/lattice.hpp:16-83).
+//
+// Bit-exact with the reference: the packed key (lattice.hpp:46-50) and the
+// murmur3 fmix64 finalizer (lattice.hpp:35-42) run on 32-bit integer
+// hardware as 64-bit wrap-around arithmetic.  Heights are produced as
+// float(corner_height) rounded to nearest: the reference's double
+// to_unit(z)*2-1 equals t * 2^-52 with t = (int64)(z ^ 2^63) >> 11 exactly,
+// so one s64->f32 conversion rounds the exact value once.
+#pragma once
+
+#include <cstdint>
+
+namespace tg {
+
+constexpr uint64_t kSeedMul = 0x9E3779B97F4A7C15ULL;  // lattice.hpp:47
+constexpr uint64_t kOctMul = 0xBF58476D1CE4E5B9ULL;   // lattice.hpp:47
+constexpr uint64_t kIxMul = 0x94D049BB133111EBULL;    // lattice.hpp:48
+constexpr uint64_t kIyMul = 0xD6E8FEB86659FD93ULL;    // lattice.hpp:49
+constexpr uint64_t kIzMul = 0xA24BAED4963EE407ULL;    // 3D extension (TG_PACK_K5, new)
+constexpr uint64_t kAngleLane = 0xA0761D6478BD642FULL;      // lattice.hpp:53
+constexpr uint64_t kMagnitudeLane = 0xE7037ED1A0B428DBULL;  // lattice.hpp:54
+
+// lattice.hpp:35-42.  Written on 32-bit halves so the SASS is exactly the
+// minimal sequence: z ^= z >> 33 only touches the low word
+// (lo ^= hi >> 1); each 64x64->64 multiply is one IMAD.WIDE.U32 plus two
+// IMAD for the cross terms.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
+    lo ^= hi >> 1;
+    {
+        const uint32_t ml = 0xED558CCDu, mh = 0xFF51AFD7u;
+        const uint64_t p = static_cast<uint64_t>(lo) * ml;
+        const uint32_t nh = static_cast<uint32_t>(p >> 32) + lo * mh + hi * ml;
+        lo = static_cast<uint32_t>(p);
+        hi = nh;
+    }
+    lo ^= hi >> 1;
+    {
+        const uint32_t ml = 0x1A85EC53u, mh = 0xC4CEB9FEu;
+        const uint64_t p = static_cast<uint64_t>(lo) * ml;
+        const uint32_t nh = static_cast<uint32_t>(p >> 32) + lo * mh + hi * ml;
+        lo = static_cast<uint32_t>(p);
+        hi = nh;
+    }
+    lo ^= hi >> 1;
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// lattice.hpp:46-50 split as pack = base + ix*K3 + iy*K4 with
+// base = seed*K1 + octave*K2 hoisted per octave.  ix/iy are signed 64-bit and
+// wrap two's-complement exactly like the reference's static_cast<uint64_t>.
+__device__ __forceinline__ uint64_t pack_xy(uint64_t base, int64_t ix, int64_t iy) {
+    return base + static_cast<uint64_t>(ix) * kIxMul + static_cast<uint64_t>(iy) * kIyMul;
+}
+
+// float(corner_height) with one round-to-nearest (lattice.hpp:56-64).
+__device__ __forceinline__ float height_from_hash(uint64_t z) {
+    const int64_t t = static_cast<int64_t>(z ^ 0x8000000000000000ULL) >> 11;
+    return __ll2float_rn(t) * 0x1p-52f;
+}
+
+// to_unit(z) = (z >> 11) * 2^-53 as float from the top 32 bits (|error| <=
+// 2^-25; used for angles and gradient magnitudes whose components are checked
+// within tolerance, not bit-exact — cos/sin are libm-dependent).
+__device__ __forceinline__ float unit_from_hash(uint64_t z) {
+    return static_cast<float>(static_cast<uint32_t>(z >> 32)) * 0x1p-32f;
+}
+
+__device__ __forceinline__ float corner_height(uint64_t base, int64_t ix, int64_t iy) {
+    return height_from_hash(mix64(pack_xy(base, ix, iy)));
+}
+
+// corner_unit_gradient (lattice.hpp:80-83): angle = unit * 2*pi, so
+// (cos, sin)(angle) = sincospi(2 * unit).
+__device__ __forceinline__ void corner_unit_gradient(uint64_t base, int64_t ix, int64_t iy,
+                                                     float* c, float* s) {
+    const uint64_t z = mix64(pack_xy(base, ix, iy) ^ kAngleLane);
+    sincospif(2.0f * unit_from_hash(z), s, c);
+}
+
+// corner_gradient (lattice.hpp:72-77): magnitude uniform in [0, w].
+__device__ __forceinline__ void corner_gradient(uint64_t base, int64_t ix, int64_t iy, float w,
+                                                float* gx, float* gy) {
+    const uint64_t p = pack_xy(base, ix, iy);
+    float c, s;
+    sincospif(2.0f * unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
+    const float m = unit_from_hash(mix64(p ^ kMagnitudeLane)) * w;
+    *gx = m * c;
+    *gy = m * s;
+}
+
+}  // namespace tg

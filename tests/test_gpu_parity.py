@@ -1,0 +1,366 @@
+"""GPU parity: the sm_100a path through the C-ABI against the oracle.
+
+Bars (BASELINE.json north_star): lattice hashes bit-exact (u64), fp32 corner
+heights equal float(reference double) exactly, heights within
+max|dh| <= 1e-5 * A (A = max |h_ref| over the window, helpers.height_tolerance),
+region/tiling/batch/shard invariance bit-exact, integer analysis results exact.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from helpers import amplitude_sum, cfg_from_dict, height_tolerance, keys_from_golden, make_cfg
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU box only
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1610_03525_b200 as pt  # noqa: E402
+from paper_1610_03525_b200 import _abi  # noqa: E402
+
+LANES = {"height": 0, "angle": 0xA0761D6478BD642F, "magnitude": 0xE7037ED1A0B428DB}
+
+
+def gen(c, ox, oy, w, h=None):
+    h = w if h is None else h
+    out = torch.empty((h, w), dtype=torch.float32, device="cuda")
+    st = _abi.load().tg_fbm_generate_rect_f32(C.byref(c), ox, oy, w, h, out.data_ptr(), w,
+                                              torch.cuda.current_stream().cuda_stream)
+    assert st == 0, _abi.last_error()
+    return out
+
+
+def check_close(got, ref, c, what=""):
+    tol = height_tolerance(ref, c)
+    err = float(np.max(np.abs(got.astype(np.float64) - ref)))
+    assert err <= tol, f"{what}: max|dh|={err:.3e} > tol={tol:.3e}"
+    return err
+
+
+# ---- lattice --------------------------------------------------------------------
+
+def _dev_keys(lat):
+    k = keys_from_golden(lat)
+    return torch.from_numpy(k.view(np.uint8).copy()).cuda(), len(k)
+
+
+def test_lattice_hash_bit_exact(golden):
+    lat = golden["lattice"]
+    dk, n = _dev_keys(lat)
+    for name, lane in LANES.items():
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        assert _abi.load().tg_lattice_hash(dk.data_ptr(), n, lane, out.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, lat[f"hash_{name}"]), name
+
+
+def test_lattice_height_is_rounded_reference(golden):
+    lat = golden["lattice"]
+    dk, n = _dev_keys(lat)
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    assert _abi.load().tg_lattice_height_f32(dk.data_ptr(), n, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), lat["height"].astype(np.float32))
+
+
+def test_lattice_unit_gradient_within_tolerance(golden):
+    lat = golden["lattice"]
+    dk, n = _dev_keys(lat)
+    out = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+    assert _abi.load().tg_lattice_unit_gradient_f32(dk.data_ptr(), n, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    g = out.cpu().numpy().reshape(-1, 2).astype(np.float64)
+    assert np.max(np.abs(g - lat["unit_gradient"])) < 1e-6
+
+
+# ---- maps against the reference's golden outputs --------------------------------
+
+def test_golden_maps(golden):
+    worst = {}
+    for name, meta in golden["maps_meta"].items():
+        ref = golden["maps"][name]
+        c = cfg_from_dict(meta["cfg"])
+        ox, oy = meta["origin"]
+        ext = meta["extent"]
+        if meta["cfg"]["normalize"]:
+            hm = pt.generate_region(pt.FbmConfig(seed=c.seed, octaves=c.octaves, resolution=c.resolution,
+                                                 base_frequency=c.base_frequency, normalize=True),
+                                    (ox, oy), ext)
+            assert hm.normalized and hm.data.min() == -1.0 and hm.data.max() == 1.0
+            got = hm.data
+        else:
+            got = gen(c, ox, oy, ext).cpu().numpy()
+        if meta["cfg"]["zero_lattice"]:
+            assert np.all(got == 0.0)
+            continue
+        worst[name] = check_close(got, ref, c, name)
+
+
+# ---- full-size BASELINE configs against the restated oracle ----------------------
+
+def _sample_check(oracle, c, dev_map, ox, oy, n=4096, seed=0):
+    h, w = dev_map.shape
+    rng = np.random.default_rng(seed)
+    ys = rng.integers(0, h, n)
+    xs = rng.integers(0, w, n)
+    ref = oracle.sample(c, xs + ox, ys + oy)
+    got = dev_map.cpu().numpy()[ys, xs].astype(np.float64)
+    tol = 1e-5 * max(float(np.max(np.abs(ref))), 1e-12)
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= tol, f"sampled max|dh|={err:.3e} > {tol:.3e}"
+
+
+def test_config1_full_map(oracle):
+    c = make_cfg(method=0, seed=1, resolution=1024, base_frequency=8, octaves=8)
+    m = gen(c, 0, 0, 1024).cpu().numpy()
+    check_close(m, oracle.generate(c, 0, 0, 1024), c, "cfg1")
+
+
+def test_config2_s5_4096(oracle):
+    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=4096, base_frequency=8, octaves=12)
+    m = gen(c, 0, 0, 4096)
+    check_close(m[:256, :256].cpu().numpy(), oracle.generate(c, 0, 0, 256), c, "cfg2 window")
+    check_close(m[-128:, -128:].cpu().numpy(), oracle.generate(c, 4096 - 128, 4096 - 128, 128), c, "cfg2 corner")
+    _sample_check(oracle, c, m, 0, 0)
+
+
+@pytest.mark.parametrize("method", [0, 1, 2, 3, 4])
+def test_config3_grid_all_methods(oracle, method):
+    c = make_cfg(method=method, seed=1, resolution=4096, base_frequency=8, octaves=12)
+    m = gen(c, 0, 0, 4096)
+    check_close(m[:128, :128].cpu().numpy(), oracle.generate(c, 0, 0, 128), c, f"cfg3 m{method}")
+    _sample_check(oracle, c, m, 0, 0, n=1024)
+
+
+def test_config5_chunk_32768(oracle):
+    # 32768^2 terrain, f0 = 32 (1024-px base cells = chunks), 16 octaves, S5.
+    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=32768, base_frequency=32, octaves=16)
+    ox, oy = 17 * 1024, 29 * 1024
+    m = gen(c, ox, oy, 1024)
+    check_close(m[:64, :64].cpu().numpy(), oracle.generate(c, ox, oy, 64), c, "cfg5 chunk")
+    _sample_check(oracle, c, m, ox, oy, n=2048)
+
+
+def test_config5_proxy_equals_golden(golden):
+    # (R=1024, f0=1) is the top-left chunk of (32768, f0=32).
+    ref = golden["maps"]["cfg5_proxy_S5"]
+    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=32768, base_frequency=32, octaves=16)
+    got = gen(c, 0, 0, 64).cpu().numpy()
+    check_close(got, ref, c, "cfg5 proxy")
+
+
+# ---- bit-exact invariants (test_fbm.cpp:256-300, acceptance C6) ------------------
+
+@pytest.mark.parametrize("method", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("ratio", [2.0, 1.7])
+def test_region_equals_submap(method, ratio):
+    c = make_cfg(method=method, seed=909, resolution=64, octaves=3, frequency_ratio=ratio)
+    full = gen(c, 0, 0, 64)
+    region = gen(c, 32, 32, 32)
+    assert torch.equal(region, full[32:, 32:])
+
+
+@pytest.mark.parametrize("method", [0, 1, 2, 3, 4])
+def test_four_way_tiling_bit_exact(method):
+    c = make_cfg(method=method, seed=2024, resolution=512, octaves=4)
+    full = gen(c, 0, 0, 512)
+    for oy in (0, 256):
+        for ox in (0, 256):
+            assert torch.equal(gen(c, ox, oy, 256), full[oy:oy + 256, ox:ox + 256])
+
+
+def test_unaligned_windows_and_shards_bit_exact():
+    # cfg2-like map cut at odd (but octave-0 aligned) origins and shapes.
+    c = make_cfg(method=0, smoothstep=5, seed=7, resolution=2048, base_frequency=64, octaves=13)
+    full = gen(c, 0, 0, 2048)
+    for ox, oy, w, h in [(32, 96, 96, 160), (1024, 0, 1024, 37), (1984, 2016, 64, 32)]:
+        assert torch.equal(gen(c, ox, oy, w, h), full[oy:oy + h, ox:ox + w])
+    # row-band shards of any count reassemble the map (multi-GPU sharding unit)
+    for n in (2, 3, 8):
+        bands = []
+        rows = [2048 * i // n // 32 * 32 for i in range(n)] + [2048]
+        for a, b in zip(rows[:-1], rows[1:]):
+            bands.append(gen(c, 0, a, 2048, b - a))
+        assert torch.equal(torch.cat(bands, 0), full)
+
+
+def test_negative_origin_region():
+    c = make_cfg(seed=3, resolution=64, octaves=4)
+    a = gen(c, 32, -32, 16)
+    b = gen(c, 0, -64, 64)
+    assert torch.equal(a, b[32:48, 32:48])
+
+
+def test_zero_source_gives_zero_map():
+    for m in (0, 2, 3):
+        c = make_cfg(method=m, resolution=16, octaves=4, zero_lattice=1)
+        assert torch.count_nonzero(gen(c, 0, 0, 16)).item() == 0
+
+
+def test_deterministic():
+    c = make_cfg(method=2, seed=777, resolution=64, octaves=4)
+    assert torch.equal(gen(c, 0, 0, 64), gen(c, 0, 0, 64))
+
+
+def test_batch_equals_single_maps():
+    c = make_cfg(method=0, smoothstep=5, seed=0, resolution=1024, base_frequency=8, octaves=8)
+    seeds = [1, 2, 99, 2**63 + 5]
+    out = torch.empty((len(seeds), 256, 256), dtype=torch.float32, device="cuda")
+    pt.generate_batch_device(pt.FbmConfig(method=0, smoothstep=5, resolution=1024, base_frequency=8, octaves=8),
+                             seeds, (256, 512), 256, 256, out)
+    for i, s in enumerate(seeds):
+        c.seed = s
+        assert torch.equal(out[i], gen(c, 256, 512, 256))
+
+
+def test_host_drop_in_matches_device():
+    cfg = pt.FbmConfig(seed=17, resolution=512, octaves=6)
+    dev = gen(cfg.to_c(), 0, 0, 512).cpu().numpy().astype(np.float64)
+    buf = np.full((512, 512), 123.0)  # stale content must be overwritten (test_fbm.cpp:375-387)
+    pt.generate_into(cfg, (0, 0), 512, buf)
+    assert np.array_equal(buf, dev)
+    hm = pt.generate_heightmap(cfg)
+    assert np.array_equal(hm.data, dev) and len(hm.octave_seconds) == 6
+    with pytest.raises(pt.ValidationError):
+        pt.generate_into(cfg, (0, 0), 512, np.zeros((511, 511)))
+    f32 = np.zeros((512, 512), np.float32)
+    pt.generate_into(cfg, (0, 0), 512, f32)
+    assert np.array_equal(f32.astype(np.float64), dev)
+
+
+def test_validation_errors_on_device_path():
+    cfg = pt.FbmConfig(resolution=64)
+    with pytest.raises(pt.ValidationError):
+        pt.generate_region(cfg, (5, 0), 16)
+    with pytest.raises(pt.ValidationError):
+        pt.generate_region(cfg, (0, 33), 16)
+    pt.generate_region(cfg, (32, -32), 16)
+
+
+def test_warnings_and_normalize():
+    hm = pt.generate_heightmap(pt.FbmConfig(resolution=8, octaves=4))
+    assert len(hm.warnings) == 1 and "octave 3" in hm.warnings[0]
+    assert pt.generate_heightmap(pt.FbmConfig(resolution=8, octaves=3)).warnings == []
+    n = pt.generate_heightmap(pt.FbmConfig(seed=21, resolution=32, octaves=3, normalize=True))
+    assert n.data.min() == -1.0 and n.data.max() == 1.0 and n.normalized
+
+
+def test_octave_sweep_amplitude_bound():
+    # |h| <= sum of per-octave kernel bounds (test_fbm.cpp:83-110, 223-237)
+    for m, per in ((0, 9.0), (3, 2.0)):
+        c = make_cfg(method=m, seed=31337, resolution=64, octaves=6)
+        v = gen(c, 0, 0, 64)
+        assert float(v.abs().max()) <= per * amplitude_sum(c)
+
+
+# ---- device normalization (fbm.hpp:638-656) ---------------------------------------
+
+def test_device_minmax_rescale(oracle):
+    c = make_cfg(seed=21, resolution=256, octaves=5)
+    m = gen(c, 0, 0, 256)
+    lo, hi = C.c_double(), C.c_double()
+    assert _abi.load().tg_minmax_f32(m.data_ptr(), m.numel(), C.byref(lo), C.byref(hi), None) == 0
+    host = m.cpu().numpy().astype(np.float64)
+    assert lo.value == host.min() and hi.value == host.max()
+    assert _abi.load().tg_rescale_f32(m.data_ptr(), m.numel(), lo.value, hi.value, None) == 0
+    torch.cuda.synchronize()
+    ref, *_ = oracle.normalize(host)
+    got = m.cpu().numpy()
+    assert got.min() == -1.0 and got.max() == 1.0
+    assert np.array_equal(got, ref.astype(np.float32))
+
+
+# ---- analysis pass --------------------------------------------------------------
+
+def test_median_exact():
+    for seed, R in ((42, 128), (5, 1000), (1, 4096)):
+        c = make_cfg(seed=seed, resolution=R, octaves=6)
+        m = gen(c, 0, 0, R)
+        med = pt.upper_median_device(m)
+        host = np.sort(m.cpu().numpy().ravel())
+        assert med == host[host.size // 2]
+
+
+def test_coastline_mask_matches_oracle(oracle):
+    c = make_cfg(seed=42, resolution=300, octaves=6)
+    m = gen(c, 0, 0, 300)
+    mask, sea, lf = pt.coastline_mask_device(m, 300)
+    host = m.cpu().numpy().astype(np.float64)
+    st, ref_mask, land = oracle.coastline_mask(host, sea)
+    assert st == 0 and np.array_equal(mask.cpu().numpy(), ref_mask)
+    assert lf == land / host.size
+
+
+def test_halfplane_and_all_land():
+    half = torch.tensor(np.where(np.arange(8)[None, :] < 4, 1.0, -1.0) * np.ones((8, 1)),
+                        dtype=torch.float32, device="cuda")
+    mask, _, lf = pt.coastline_mask_device(half.contiguous(), 8, 0.0)
+    expect = np.zeros((8, 8), np.uint8)
+    expect[:, 3] = 1
+    assert np.array_equal(mask.cpu().numpy(), expect) and lf == 0.5
+    with pytest.raises(pt.ValidationError):
+        pt.coastline_mask_device(torch.full((4, 4), 2.0, device="cuda"), 4, 0.0)
+
+
+def test_box_count_known_answers():
+    col = torch.zeros((64, 64), dtype=torch.uint8, device="cuda")
+    col[:, 31] = 1
+    r = pt.box_count_mask_device(col, 64, [2, 4, 8, 16])
+    assert r.counts == [32, 16, 8, 4] and abs(r.d - 1.0) < 1e-12 and abs(r.k - 64.0) < 1e-9
+    r = pt.box_count_mask_device(torch.ones((64, 64), dtype=torch.uint8, device="cuda"), 64, [2, 4, 8, 16])
+    assert r.counts == [1024, 256, 64, 16] and abs(r.d - 2.0) < 1e-12
+    with pytest.raises(pt.ValidationError):
+        pt.box_count_mask_device(col, 64, [2, 4])
+    with pytest.raises(pt.ValidationError):
+        pt.box_count_mask_device(col, 64, [4, 2, 8])
+    with pytest.raises(pt.ValidationError):
+        pt.box_count_mask_device(torch.zeros((8, 8), dtype=torch.uint8, device="cuda"), 8, [2, 4, 8])
+
+
+@pytest.mark.parametrize("R,sizes", [(512, [2, 4, 8, 16, 32, 64]), (1000, [3, 5, 7, 33, 100]),
+                                     (4096, [2, 4, 8, 16, 32, 64])])
+def test_fused_boxcount_matches_oracle(oracle, R, sizes):
+    c = make_cfg(method=0, smoothstep=5, seed=42, resolution=R, base_frequency=8, octaves=8)
+    m = gen(c, 0, 0, R)
+    rep = pt.box_count_device(m, R, sizes)
+    host = m.cpu().numpy().astype(np.float64)
+    assert rep.sea_level == oracle.upper_median(host)
+    st, mask, land = oracle.coastline_mask(host, rep.sea_level)
+    st, counts, d, k, r2 = oracle.box_count(mask, sizes)
+    assert list(counts) == rep.counts
+    assert rep.coast_pixels == int(mask.sum()) and rep.land_fraction == land / host.size
+    assert abs(rep.d - d) < 1e-12 and abs(rep.r2 - r2) < 1e-12
+
+
+def test_variogram_matches_oracle(oracle):
+    c = make_cfg(method=0, smoothstep=5, seed=3, resolution=512, base_frequency=8, octaves=10)
+    m = gen(c, 0, 0, 512)
+    lags = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
+    ss, pr = pt.variogram_device(m, 512, 512, lags)
+    rss, rpr = oracle.variogram(m.cpu().numpy().astype(np.float64), lags)
+    assert np.array_equal(pr, rpr)
+    assert np.allclose(ss, rss, rtol=1e-10, atol=0)
+
+
+# ---- 3D (new; property-pinned + restated oracle) ------------------------------------
+
+def test_fbm3d_matches_restated_oracle(oracle):
+    c = make_cfg(method=1, seed=5, resolution=64, base_frequency=8, octaves=5)
+    out = torch.empty((64, 64, 64), dtype=torch.float32, device="cuda")
+    pt.generate3d_device(pt.FbmConfig(method=1, seed=5, resolution=64, base_frequency=8, octaves=5),
+                         (0, 0, 0), (64, 64, 64), out)
+    ref = oracle.generate3d(c, 0, 0, 0, 64, 64, 64)
+    check_close(out.cpu().numpy(), ref, c, "3d")
+
+
+def test_fbm3d_subvolume_bit_exact():
+    cfg = pt.FbmConfig(method=1, seed=9, resolution=128, base_frequency=4, octaves=7, smoothstep=5)
+    full = torch.empty((128, 128, 128), dtype=torch.float32, device="cuda")
+    pt.generate3d_device(cfg, (0, 0, 0), (128, 128, 128), full)
+    sub = torch.empty((32, 64, 96), dtype=torch.float32, device="cuda")
+    pt.generate3d_device(cfg, (32, 64, 96), (32, 64, 96), sub)
+    assert torch.equal(sub, full[96:128, 64:128, 32:128])
