@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpolyterrain_b200.so")
+LIB_PATH = os.environ.get("TG_LIB_PATH") or os.path.join(HERE, "lib", "libpolyterrain_b200.so")
 
 TG_OK, TG_EVALIDATION, TG_EIO, TG_ENUMERICAL, TG_EDEVICE = 0, 1, 2, 3, 4
 

@@ -32,14 +32,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          extra: list | None = None) -> str:
+    """Compile SOURCES into `out` (default: the in-tree library)."""
+    target = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd))
@@ -49,16 +52,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out.stderr:
             print(out.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    tmp = target + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"link failed:\n{out.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     for o in objs:
         os.remove(o)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    # python -m paper_1610_03525_b200.build [--verbose] [--out PATH] [-DNAME=V ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else None
+    extra = [a for a in argv if a.startswith("-D")]
+    print(build(force=True, verbose="--verbose" in argv, out=out, extra=extra))

@@ -258,7 +258,7 @@ int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* str
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Scratch scr(s);
-    cudaError_t e = scr.alloc(sizeof(SelectState) + kBins * sizeof(unsigned long long));
+    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long));
     if (e != cudaSuccess) return set_cuda_error(e, "median alloc");
     SelectState* state = static_cast<SelectState*>(scr.p);
     unsigned long long* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);

@@ -26,6 +26,7 @@ void fbm3d_tile(int* tx, int* ty, int* tz);
 cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uint64_t lane,
                            void* out, cudaStream_t st);
 cudaError_t widen_launch(const float* in, double* out, uint64_t n, cudaStream_t st);
+const float4* row_lut(int order);
 }  // namespace tg
 
 namespace {
@@ -89,10 +90,15 @@ void octave_spec(const tg_fbm_config* c, int octave, tg_octave_spec* os) {
 }
 
 // Fill the per-octave device plan for windows whose global coordinates stay
-// within |g| <= gmax.
-void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out) {
+// within |g| <= gmax: sampling class, evaluation mode and the per-CTA
+// shared-memory layout (fbm2d.cu).  Every decision depends on the
+// configuration only, so all windows of one map evaluate each octave the same
+// way (fbm.hpp:7-8).
+void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool plan_2d) {
     const double R = static_cast<double>(c->resolution);
     const double w = c->has_gradient_weight ? c->gradient_weight : c->base_amplitude / 100.0;
+    const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
+    int goff = 0, slot = 0;
     for (int o = 0; o < c->octaves; ++o) {
         tg_octave_spec os;
         octave_spec(c, o, &os);
@@ -103,6 +109,8 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out) {
         d.amp = static_cast<float>(os.amp);
         d.w = static_cast<float>(w);
         d.shift = -1;
+        d.tslot = -1;
+        d.lut_off = -1;
         if (os.fast) {
             d.cls = tg::kClsFast;
             d.ppc = os.ppc;
@@ -112,23 +120,65 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out) {
                 while ((1LL << s) < os.ppc) ++s;
                 d.shift = s;
             }
-            continue;
-        }
-        d.cls = tg::kClsGeneral;
-        // Exact lattice-point sampling: R = 2^n and freq = k*R with k even make
-        // ((g + 0.5)/R)*freq = g*k + k/2 exactly in fp64 (no rounding while
-        // |g*k| < 2^52), so render_general sees cx = cy = 0 (fbm.hpp:468-489).
-        if (is_pow2(c->resolution)) {
-            const double kd = os.freq / R;
-            if (kd >= 2.0 && kd < 9.0e15 && std::floor(kd) == kd && kd * R == os.freq) {
-                const int64_t k = static_cast<int64_t>(kd);
-                const double bound = (static_cast<double>(gmax) + 1.0) * kd + kd;
-                if ((k & 1) == 0 && bound < 4.0e15) {
-                    d.cls = tg::kClsSubInt;
-                    d.k = k;
+        } else {
+            d.cls = tg::kClsGeneral;
+            // Exact lattice-point sampling: R = 2^n and freq = k*R with k even make
+            // ((g + 0.5)/R)*freq = g*k + k/2 exactly in fp64 (no rounding while
+            // |g*k| < 2^52), so render_general sees cx = cy = 0 (fbm.hpp:468-489).
+            if (is_pow2(c->resolution)) {
+                const double kd = os.freq / R;
+                if (kd >= 2.0 && kd < 9.0e15 && std::floor(kd) == kd && kd * R == os.freq) {
+                    const int64_t k = static_cast<int64_t>(kd);
+                    const double bound = (static_cast<double>(gmax) + 1.0) * kd + kd;
+                    if ((k & 1) == 0 && bound < 4.0e15) {
+                        d.cls = tg::kClsSubInt;
+                        d.k = k;
+                    }
                 }
             }
         }
+        if (!plan_2d) continue;
+        if (d.cls == tg::kClsSubInt) {
+            d.mode = tg::kModeSubInt;
+            continue;
+        }
+        int64_t ncx, ncy;
+        int mode;
+        if (d.cls == tg::kClsFast && d.shift >= 0 && d.shift <= tg::kLutLog2Max) {
+            d.lut_off = (1 << d.shift) - 1;
+            ncx = std::max<int64_t>(tg::kTileW >> d.shift, 1) + 1;
+            ncy = std::max<int64_t>(tg::kTileH >> d.shift, 1) + 1;
+            if (zg && d.ppc == 1) mode = tg::kModePpc1;
+            else if (zg && d.ppc == 2) mode = tg::kModeBlock2;
+            else if (d.ppc >= 4) mode = tg::kModeBlock;
+            else mode = tg::kModeGrid;
+        } else if (d.cls == tg::kClsFast) {
+            // tile spans at most floor(127/ppc) + 2 cells
+            ncx = (tg::kTileW - 1) / d.ppc + 3;
+            ncy = (tg::kTileH - 1) / d.ppc + 3;
+            mode = tg::kModeGrid;
+        } else {
+            const double span = d.freq / R;
+            const double bx = std::ceil((tg::kTileW - 1) * span) + 3.0;
+            const double by = std::ceil((tg::kTileH - 1) * span) + 3.0;
+            ncx = bx > 1.0e6 ? 1000000 : static_cast<int64_t>(bx);
+            ncy = by > 1.0e6 ? 1000000 : static_cast<int64_t>(by);
+            mode = tg::kModeGrid;
+        }
+        const int64_t pitch = (ncx + 3) & ~int64_t(3);
+        const int64_t size = pitch * ncy;
+        const bool needs_tab = mode == tg::kModeGrid;
+        if (ncx * ncy > tg::kGridCap || goff + size > tg::kGridCap || (needs_tab && slot >= tg::kTabSlots)) {
+            d.mode = tg::kModeDirect;
+            continue;
+        }
+        d.mode = mode;
+        d.ncx = static_cast<int32_t>(ncx);
+        d.ncy = static_cast<int32_t>(ncy);
+        d.pitch = static_cast<int32_t>(pitch);
+        d.goff = goff;
+        goff += static_cast<int>(size);
+        if (needs_tab) d.tslot = slot++;
     }
 }
 
@@ -201,7 +251,9 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     int64_t gmax = 0;
     const int64_t cand[4] = {ox - 256, ox + width + 256, oy - 256, oy + height + 256};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
-    plan_octaves(c, gmax, a->oct);
+    plan_octaves(c, gmax, a->oct, true);
+    a->lut = tg::row_lut(order_of(c));
+    if (!a->lut) return fail(TG_EDEVICE, "row LUT allocation failed");
     return TG_OK;
 }
 
@@ -246,7 +298,7 @@ int tg_fbm_generate_rect_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, i
     if (ld < width) return fail(TG_EVALIDATION, "generate: row pitch smaller than width");
     if (int st = device_ready()) return st;
     tg::FbmArgs a;
-    build_args(cfg, ox, oy, width, height, ld, &a);
+    if (int st = build_args(cfg, ox, oy, width, height, ld, &a)) return st;
     TG_CUDA(tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, dev_out,
                              static_cast<cudaStream_t>(stream)));
     return TG_OK;
@@ -270,7 +322,7 @@ int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, i
     if (!seeds || n_seeds < 1 || !dev_out) return fail(TG_EVALIDATION, "batch: bad arguments");
     if (int st = device_ready()) return st;
     tg::FbmArgs a;
-    build_args(cfg, ox, oy, width, height, width, &a);
+    if (int st = build_args(cfg, ox, oy, width, height, width, &a)) return st;
     for (int32_t b0 = 0; b0 < n_seeds; b0 += tg::kMaxBatch) {
         const int nb = std::min<int32_t>(tg::kMaxBatch, n_seeds - b0);
         a.n_maps = nb;
@@ -321,7 +373,10 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
         int bi = 0;
         for (int64_t y0 = 0; y0 < extent && rc == TG_OK; y0 += band, bi ^= 1) {
             const int64_t h = std::min<int64_t>(band, extent - y0);
-            build_args(cfg, ox, oy + y0, extent, h, extent, &a);
+            if (build_args(cfg, ox, oy + y0, extent, h, extent, &a) != TG_OK) {
+                rc = TG_EDEVICE;
+                break;
+            }
             cudaError_t e = tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, dev32[bi], st[bi]);
             const void* src = dev32[bi];
             if (e == cudaSuccess && f64) {
@@ -386,7 +441,7 @@ int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int6
     int64_t gmax = 0;
     const int64_t cand[6] = {ox - 64, ox + nx + 64, oy - 64, oy + ny + 64, oz - 64, oz + nz + 64};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
-    plan_octaves(cfg, gmax, a.oct);
+    plan_octaves(cfg, gmax, a.oct, false);
     TG_CUDA(tg::fbm3d_launch(order_of(cfg), a, dev_out, static_cast<cudaStream_t>(stream)));
     return TG_OK;
 }

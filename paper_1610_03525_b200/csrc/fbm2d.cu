@@ -8,16 +8,16 @@
 // (4 B/pixel) instead of the reference's read-modify-write of a double buffer
 // per octave (fbm.hpp:187,193).
 //
-// Per octave the CTA
-//   (A) builds column/row sampling tables (cell index, x, S(x)) and hashes the
-//       tile's unique lattice corners once into shared memory;
-//   (B) every thread evaluates its 4 x RPT pixels from the shared corners with
-//       the cell polynomial factorised per (cell, row):
-//         zg paper     v = c0 + sx*c1 + x*c2      (kernels2d.hpp:62-76)
-//         zg separable v = c0 + sx*c1
-//         perlin       v = a0 + x*a1 + sx*a2 + x*sx*a3   (kernels2d.hpp:163-173)
-//         generic      v = ((r3*x + r2)*x + r1)*x + r0    (kernels2d.hpp:124-134)
-// Octaves whose samples sit exactly on lattice points (kClsSubInt) skip the
+// The CTA runs one prologue for ALL octaves — sampling tables (cell index,
+// x, S(x)) and every octave's unique lattice corners hashed once into shared
+// memory — then a barrier-free octave loop in which each thread evaluates its
+// 4 x 8 pixels from the shared corners, with the cell polynomial factorised
+// per (cell, row):
+//   zg paper     v = c0 + sx*c1 + x*c2      (kernels2d.hpp:62-76)
+//   zg separable v = c0 + sx*c1
+//   perlin       v = a0 + x*a1 + sx*a2 + x*sx*a3   (kernels2d.hpp:163-173)
+//   generic      v = ((r3*x + r2)*x + r1)*x + r0    (kernels2d.hpp:124-134)
+// Octaves whose samples sit exactly on lattice points (kClsSubInt) need no
 // tables: each pixel hashes its one corner in registers.
 //
 // Every pixel's arithmetic is a function of (config, global pixel) only, so
@@ -44,28 +44,39 @@ template <> struct Traits<kZgSeparable> { static constexpr int kCh = 1; };
 template <> struct Traits<kPerlin> { static constexpr int kCh = 2; };
 template <> struct Traits<kGeneric> { static constexpr int kCh = 3; };
 
-// Corner data of one lattice point, already scaled like the reference's
-// render paths: zg/generic heights x amp (fbm.hpp:270,349), Perlin unit
-// gradients x amp (409-420), generic gradients unscaled (348).
+// Corner data of one lattice point from its packed key (lattice.hpp:46-50),
+// already scaled like the reference's render paths: zg/generic heights x amp
+// (fbm.hpp:270,349), Perlin unit gradients x amp (409-420), generic gradients
+// unscaled (348).  amp63 = amp * 2^-63 (see height_scaled_from_pre).
 template <int KIND>
-__device__ __forceinline__ void corner_data(uint64_t base, int64_t ix, int64_t iy, float amp,
-                                            float w, int zero, float* d) {
+__device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float amp63, float w,
+                                                   int zero, float* d) {
     if (zero) {
 #pragma unroll
         for (int c = 0; c < Traits<KIND>::kCh; ++c) d[c] = 0.f;
         return;
     }
     if constexpr (KIND == kZgPaper || KIND == kZgSeparable) {
-        d[0] = amp * corner_height(base, ix, iy);
+        d[0] = amp63 * height_scaled(p);
     } else if constexpr (KIND == kPerlin) {
         float c, s;
-        corner_unit_gradient(base, ix, iy, &c, &s);
+        sincospif(2.0f * unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
         d[0] = amp * c;
         d[1] = amp * s;
     } else {
-        d[0] = amp * corner_height(base, ix, iy);
-        corner_gradient(base, ix, iy, w, &d[1], &d[2]);
+        d[0] = amp63 * height_scaled(p);
+        float c, s;
+        sincospif(2.0f * unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
+        const float m = unit_from_hash(mix64(p ^ kMagnitudeLane)) * w;
+        d[1] = m * c;
+        d[2] = m * s;
     }
+}
+
+template <int KIND>
+__device__ __forceinline__ void corner_data(uint64_t base, int64_t ix, int64_t iy, float amp,
+                                            float w, int zero, float* d) {
+    corner_data_packed<KIND>(pack_xy(base, ix, iy), amp, amp * 0x1p-63f, w, zero, d);
 }
 
 // Per-cell constants (from the 4 corners) and per-(cell,row) coefficients.
@@ -196,173 +207,451 @@ __device__ __forceinline__ void axis_coord(const OctDev& od, double R, int64_t g
     }
 }
 
-template <int RPT>
-struct SmemFixed {
+constexpr int kTH = kTileH;
+
+struct TabSlot {
     float colX[kTW], colS[kTW], colXS[kTW];
-    int64_t colI[kTW];
-    float rowY[8 * RPT], rowS[8 * RPT];
-    int64_t rowI[8 * RPT];
+    int32_t colI[kTW];  // cell index relative to the tile's first cell
+    float4 rowF[kTH];   // y, S(y), S(y) - y, cell row relative (bits)
 };
 
-template <int RPT>
-constexpr int grid_capacity() {
-    return ((kTW + 2) * (8 * RPT + 2) + 63) / 64 * 64;
-}
-
-template <int KIND, int RPT>
+template <int KIND>
 constexpr size_t smem_bytes() {
-    return sizeof(SmemFixed<RPT>) + sizeof(float) * Traits<KIND>::kCh * grid_capacity<RPT>();
+    return sizeof(TabSlot) * kTabSlots + sizeof(float) * Traits<KIND>::kCh * kGridCap;
 }
 
-template <int KIND, int ORDER, int RPT>
-__global__ void __launch_bounds__(kThreads)
+// 0.25*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
+// rows r = 0..8 of a 5-wide corner strip: x = y = 0.5 makes every zero-
+// gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners.
+template <class Fetch>
+__device__ __forceinline__ void ppc1_block(float (&acc)[8][4], Fetch fetch) {
+    float h[5];
+    fetch(0, h);
+    float hs[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        fetch(r + 1, h);
+        const float ns[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc[r][j] = fmaf(0.25f, hs[j] + ns[j], acc[r][j]);
+            hs[j] = ns[j];
+        }
+    }
+}
+
+template <int KIND, int ORDER>
+#ifndef TG_ZG_MIN_BLOCKS
+#define TG_ZG_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kThreads, (KIND == kZgPaper || KIND == kZgSeparable) ? TG_ZG_MIN_BLOCKS : 1)
 fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
-    constexpr int TH = 8 * RPT;
     constexpr int CH = Traits<KIND>::kCh;
-    constexpr int CAP = grid_capacity<RPT>();
+    constexpr bool kZg = KIND == kZgPaper || KIND == kZgSeparable;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SmemFixed<RPT>& S = *reinterpret_cast<SmemFixed<RPT>*>(smem_raw);
-    float* grid = reinterpret_cast<float*>(smem_raw + sizeof(SmemFixed<RPT>));
+    TabSlot* tabs = reinterpret_cast<TabSlot*>(smem_raw);
+    float* grid = reinterpret_cast<float*>(smem_raw + sizeof(TabSlot) * kTabSlots);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const int64_t tx0 = args.tile_x0 + static_cast<int64_t>(blockIdx.x) * kTW;
-    const int64_t ty0 = args.tile_y0 + static_cast<int64_t>(blockIdx.y) * TH;
+    const int64_t ty0 = args.tile_y0 + static_cast<int64_t>(blockIdx.y) * kTH;
     const int map = blockIdx.z;
     const uint64_t seed_key = args.seed_key[map];
     const int c0 = lane * 4;
-    const int r0 = warp * RPT;
+    const int r0 = warp * 8;
+    const int nocts = args.octaves;
 
-    float acc[RPT][4];
+    // ---- prologue: every octave's tile corners (and, for general octaves,
+    // sampling tables) into shared memory; one barrier for the whole kernel.
+    // Coarse aligned octaves (<= 32 corners per tile) first: one warp per
+    // octave, one corner per lane.
+    for (int o = warp; o < nocts; o += kThreads / 32) {
+        const OctDev& od = args.oct[o];
+        if (od.mode == kModeSubInt || od.mode == kModeDirect || od.lut_off < 0 || od.ncx * od.ncy > 32)
+            continue;
+        if (lane < od.ncx * od.ncy) {
+            const int cy = lane / od.ncx, cx = lane - cy * od.ncx;
+            const uint64_t p = pack_xy(seed_key + od.oct_key, (tx0 >> od.shift) + cx, (ty0 >> od.shift) + cy);
+            float d[CH];
+            corner_data_packed<KIND>(p, od.amp, od.amp * 0x1p-63f, od.w, args.zero, d);
 #pragma unroll
-    for (int r = 0; r < RPT; ++r)
+            for (int c = 0; c < CH; ++c) grid[c * kGridCap + od.goff + cy * od.pitch + cx] = d[c];
+        }
+    }
+    for (int o = 0; o < nocts; ++o) {
+        const OctDev& od = args.oct[o];
+        const int mode = od.mode;
+        if (mode == kModeSubInt || mode == kModeDirect) continue;
+        if (od.lut_off >= 0 && od.ncx * od.ncy <= 32 && mode != kModeGrid) continue;  // done above
+        const uint64_t base = seed_key + od.oct_key;
+        const bool aligned = od.lut_off >= 0;  // power-of-two ppc on the aligned tile grid
+        int64_t ix0, iy0;
+        int ncx = od.ncx, ncy = od.ncy;
+        if (aligned) {
+            ix0 = tx0 >> od.shift;
+            iy0 = ty0 >> od.shift;
+        } else {
+            int64_t ixe, iye;
+            float t;
+            axis_coord(od, args.R, tx0, &ix0, &t);
+            axis_coord(od, args.R, ty0, &iy0, &t);
+            axis_coord(od, args.R, tx0 + kTW - 1, &ixe, &t);
+            axis_coord(od, args.R, ty0 + kTH - 1, &iye, &t);
+            ncx = static_cast<int>(ixe - ix0 + 2);  // <= the planned bound
+            ncy = static_cast<int>(iye - iy0 + 2);
+        }
+        if (mode == kModeGrid) {
+            TabSlot& tb = tabs[od.tslot];
+            if (tid < kTW) {
+                int64_t i;
+                float x;
+                axis_coord(od, args.R, tx0 + tid, &i, &x);
+                const float sx = smooth<ORDER>(x);
+                tb.colI[tid] = static_cast<int32_t>(i - ix0);
+                tb.colX[tid] = x;
+                tb.colS[tid] = sx;
+                tb.colXS[tid] = x * sx;
+            } else if (tid < kTW + kTH) {
+                const int r = tid - kTW;
+                int64_t i;
+                float y;
+                axis_coord(od, args.R, ty0 + r, &i, &y);
+                const float sy = smooth<ORDER>(y);
+                tb.rowF[r] = make_float4(y, sy, sy - y, __int_as_float(static_cast<int32_t>(i - iy0)));
+            }
+        }
+        const int pitch = od.pitch;
+        const uint64_t p0 = pack_xy(base, ix0, iy0);
+        const float amp = od.amp, amp63 = od.amp * 0x1p-63f, w = od.w;
+        float* g = grid + od.goff;
+        if (CH == 1 && aligned && od.shift <= 4) {
+            // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc.  The main
+            // block goes 4 consecutive corners per lane (four independent hash
+            // chains, keys advanced by +K3, one 16-byte store); the last column
+            // and row go through the flat loop.
+            const int sh = od.shift;
+            const int Wm = kTW >> sh, Hm = kTH >> sh;
+            const int lsh = 5 - sh;            // log2(lanes per corner row) = log2(Wm / 4)
+            const int cg = lane & ((1 << lsh) - 1), rs = lane >> lsh;
+            const int rstep = (kThreads / 32) << sh;  // rows per pass over all warps
+            const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
+            for (int cy = (warp << sh) + rs; cy < Hm; cy += rstep) {
+                const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
+                float4 v;
+                v.x = amp63 * height_scaled(p);
+                v.y = amp63 * height_scaled(p + kIxMul);
+                v.z = amp63 * height_scaled(p + 2 * kIxMul);
+                v.w = amp63 * height_scaled(p + 3 * kIxMul);
+                if (args.zero) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = v;
+            }
+            for (int i = tid; i < Hm + 1 + Wm; i += kThreads) {
+                const int cx = i <= Hm ? Wm : i - Hm - 1;
+                const int cy = i <= Hm ? i : Hm;
+                const uint64_t p = p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                                   static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
+                float d[CH];
+                corner_data_packed<KIND>(p, amp, amp63, w, args.zero, d);
+                g[cy * pitch + cx] = d[0];
+            }
+        } else {
+            // Any other shape: flat corner list, four hash chains per thread.
+            const int n = ncx * ncy;
+            const float rcp = 1.0f / static_cast<float>(ncx);
+            for (int i0 = tid; i0 < n; i0 += 4 * kThreads) {
+                float d[4][CH];
+                int dst[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = min(i0 + u * kThreads, n - 1);
+                    const int cy = static_cast<int>((static_cast<float>(i) + 0.5f) * rcp);
+                    const int cx = i - cy * ncx;
+                    dst[u] = cy * pitch + cx;
+                    const uint64_t p = p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                                       static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
+                    corner_data_packed<KIND>(p, amp, amp63, w, args.zero, d[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (i0 + u * kThreads < n) {
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) g[c * kGridCap + dst[u]] = d[u][c];
+                    }
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- per-octave evaluation of the thread's 4 x 8 pixels (no barriers) ---
+    float acc[8][4];
+    float racc[8];  // per-row terms common to the 4 columns (zg block mode)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        racc[r] = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
+    }
 
-    for (int o = 0; o < args.octaves; ++o) {
+    for (int o = 0; o < nocts; ++o) {
         const OctDev& od = args.oct[o];
+        const int mode = od.mode;
         const uint64_t base = seed_key + od.oct_key;
-        const float amp = od.amp;
 
-        if (od.cls == kClsSubInt) {
-            // Samples on lattice points: zg and generic contribute h(ix, iy)
+        if (mode == kModeSubInt) {
+            // Lattice-point samples: zg and generic contribute h(ix, iy)
             // exactly, Perlin exactly 0 (SURVEY §8c "exact shortcuts").
             if (KIND == kPerlin || args.zero) continue;
+            const float amp = od.amp * 0x1p-63f;  // exact power-of-two rescale
             const int64_t k = od.k, half = od.k >> 1;
             uint64_t X[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 X[j] = static_cast<uint64_t>((tx0 + c0 + j) * k + half) * kIxMul;
+            uint64_t Y = base + static_cast<uint64_t>((ty0 + r0) * k + half) * kIyMul;
+            const uint64_t dY = static_cast<uint64_t>(k) * kIyMul;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                const uint64_t Y =
-                    base + static_cast<uint64_t>((ty0 + r0 + r) * k + half) * kIyMul;
+            for (int r = 0; r < 8; ++r) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    acc[r][j] = fmaf(amp, height_from_hash(mix64(X[j] + Y)), acc[r][j]);
+                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, height_scaled(X[j] + Y), acc[r][j]);
+                Y += dY;
             }
             continue;
         }
 
-        // ---- (A) sampling tables + unique corners of this tile -------------
-        __syncthreads();  // previous octave finished reading shared memory
-        if (tid < kTW) {
-            int64_t i;
-            float t;
-            axis_coord(od, args.R, tx0 + tid, &i, &t);
-            const float s = smooth<ORDER>(t);
-            S.colI[tid] = i;
-            S.colX[tid] = t;
-            S.colS[tid] = s;
-            S.colXS[tid] = t * s;
-        } else if (tid - kTW < TH) {
-            const int r = tid - kTW;
-            int64_t i;
-            float t;
-            axis_coord(od, args.R, ty0 + r, &i, &t);
-            S.rowI[r] = i;
-            S.rowY[r] = t;
-            S.rowS[r] = smooth<ORDER>(t);
-        }
-        int64_t ix0, iy0, ixe, iye;
-        float dummy;
-        axis_coord(od, args.R, tx0, &ix0, &dummy);
-        axis_coord(od, args.R, tx0 + kTW - 1, &ixe, &dummy);
-        axis_coord(od, args.R, ty0, &iy0, &dummy);
-        axis_coord(od, args.R, ty0 + TH - 1, &iye, &dummy);
-        const int64_t ncx64 = ixe - ix0 + 2, ncy64 = iye - iy0 + 2;
-        const bool direct = ncx64 * ncy64 > CAP;
-        const int ncx = static_cast<int>(ncx64), ncy = static_cast<int>(ncy64);
-        if (!direct) {
-            for (int cy = warp; cy < ncy; cy += kThreads / 32)
-                for (int cx = lane; cx < ncx; cx += 32) {
-                    float d[CH];
-                    corner_data<KIND>(base, ix0 + cx, iy0 + cy, amp, od.w, args.zero, d);
+        if constexpr (kZg) {
+            if (mode == kModePpc1) {
+                const float* g = grid + od.goff + r0 * od.pitch + c0;
+                const int pitch = od.pitch;
+                ppc1_block(acc, [&](int r, float (&h)[5]) {
+                    const float4 v = *reinterpret_cast<const float4*>(g + r * pitch);
+                    h[0] = v.x;
+                    h[1] = v.y;
+                    h[2] = v.z;
+                    h[3] = v.w;
+                    h[4] = g[r * pitch + 4];
+                });
+                continue;
+            }
+            if (mode == kModeBlock2) {
+                // 2 px per cell: columns (0,1) | (2,3) are two cells at x = 0.25,
+                // 0.75; rows pair up the same way.  3 corners per corner row.
+                const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
+                const int pitch = od.pitch;
+                const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
+                float t0 = g[0], t1 = g[1], t2 = g[2];
 #pragma unroll
-                    for (int c = 0; c < CH; ++c) grid[c * CAP + cy * ncx + cx] = d[c];
+                for (int q = 0; q < 4; ++q) {
+                    const float* gn = g + (q + 1) * pitch;
+                    const float b0 = gn[0], b1 = gn[1], b2 = gn[2];
+                    Cell<KIND> ca, cb;
+                    ca.make(&t0, &t1, &b0, &b1);
+                    cb.make(&t1, &t2, &b1, &b2);
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const float4 f = rr ? e1 : e0;
+                        const auto ra = ca.row(f.x, f.y);
+                        const auto rb = cb.row(f.x, f.y);
+                        const int r = 2 * q + rr;
+                        acc[r][0] += Cell<KIND>::eval(ra, e0.x, e0.y, e0.w);
+                        acc[r][1] += Cell<KIND>::eval(ra, e1.x, e1.y, e1.w);
+                        acc[r][2] += Cell<KIND>::eval(rb, e0.x, e0.y, e0.w);
+                        acc[r][3] += Cell<KIND>::eval(rb, e1.x, e1.y, e1.w);
+                    }
+                    t0 = b0;
+                    t1 = b1;
+                    t2 = b2;
                 }
+                continue;
+            }
         }
-        __syncthreads();
 
-        // ---- (B) evaluate the thread's 4 x RPT pixels ----------------------
-        float x[4], sx[4], xs[4];
-        int64_t cxi[4];
+        if (mode == kModeBlock) {
+            // Power-of-two ppc >= 4 on the aligned tile grid: the thread's 4
+            // columns share one cell; its 8 rows change cell row only every ppc
+            // rows (never when ppc >= 8).  Sampling values from the row LUT.
+            const int sh = od.shift, mask = od.ppc - 1;
+            const float4* L = args.lut + od.lut_off;
+            const int xo = static_cast<int>(tx0 & mask) + c0;
+            const int yo = static_cast<int>(ty0 & mask) + r0;
+            const int pitch = od.pitch;
+            const float* g = grid + od.goff + (xo >> sh);
+            float x[4], sx[4], xs[4];
+            const float4* Lx = L + (xo & mask);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            x[j] = S.colX[c0 + j];
-            sx[j] = S.colS[c0 + j];
-            xs[j] = S.colXS[c0 + j];
-            cxi[j] = S.colI[c0 + j];
+            for (int j = 0; j < 4; ++j) {
+                const float4 e = Lx[j];
+                x[j] = e.x;
+                sx[j] = e.y;
+                xs[j] = e.w;
+            }
+            if constexpr (kZg) {
+                // v = c0 + sx*c1 (+ x*c2): c0 is common to the 4 columns and goes
+                // into the per-row accumulator once per row.
+                const float4* Ly = L + (yo & mask);
+                const float* q = g + (yo >> sh) * pitch;
+                if (sh >= 3) {
+                    // ppc >= 8: the 4 x 8 block lies in one cell
+                    float h00, h10, h01, h11;
+                    h00 = q[0];
+                    h10 = q[1];
+                    h01 = q[pitch];
+                    h11 = q[pitch + 1];
+                    const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const float4 f = Ly[r];
+                        racc[r] += fmaf(f.y, dy, h00);
+                        if constexpr (KIND == kZgPaper) {
+                            const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j]));
+                        } else {
+                            const float c1 = fmaf(a, f.y, dx);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(sx[j], c1, acc[r][j]);
+                        }
+                    }
+                } else {
+                    // ppc == 4: rows 0-3 and 4-7 are two cell rows
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const float* qh = q + half * pitch;
+                        const float h00 = qh[0], h10 = qh[1], h01 = qh[pitch], h11 = qh[pitch + 1];
+                        const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+#pragma unroll
+                        for (int rr = 0; rr < 4; ++rr) {
+                            const int r = 4 * half + rr;
+                            const float4 f = L[rr];
+                            racc[r] += fmaf(f.y, dy, h00);
+                            if constexpr (KIND == kZgPaper) {
+                                const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j]));
+                            } else {
+                                const float c1 = fmaf(a, f.y, dx);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(sx[j], c1, acc[r][j]);
+                            }
+                        }
+                    }
+                }
+            } else {
+                Cell<KIND> cell;
+                int last = -1;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int yr = yo + r;
+                    const int ry = yr >> sh;
+                    const float4 f = L[yr & mask];
+                    if (ry != last) {
+                        const int key = ry * pitch;
+                        float k00[CH], k10[CH], k01[CH], k11[CH];
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            k00[c] = g[c * kGridCap + key];
+                            k10[c] = g[c * kGridCap + key + 1];
+                            k01[c] = g[c * kGridCap + key + pitch];
+                            k11[c] = g[c * kGridCap + key + pitch + 1];
+                        }
+                        cell.make(k00, k10, k01, k11);
+                        last = ry;
+                    }
+                    const auto row = cell.row(f.x, f.y);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
+                }
+            }
+            continue;
         }
-        const bool one_cell = cxi[0] == cxi[3];
-        int last_key = -1;
-        Cell<KIND> cell;
+
+        if (mode == kModeGrid) {
+            const TabSlot& tb = tabs[od.tslot];
+            const float* g = grid + od.goff;
+            const int pitch = od.pitch;
+            float x[4], sx[4], xs[4];
+            int cxi[4];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-            const float y = S.rowY[r0 + r];
-            const float sy = S.rowS[r0 + r];
-            const int64_t iy = S.rowI[r0 + r];
-            if (!direct) {
-                const int ry = static_cast<int>(iy - iy0);
+            for (int j = 0; j < 4; ++j) {
+                x[j] = tb.colX[c0 + j];
+                sx[j] = tb.colS[c0 + j];
+                xs[j] = tb.colXS[c0 + j];
+                cxi[j] = tb.colI[c0 + j];
+            }
+            const bool one_cell = cxi[0] == cxi[3];
+            int last_key = -1;
+            Cell<KIND> cell;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const float4 f = tb.rowF[r0 + r];
+                const float y = f.x, sy = f.y;
+                const int ry = __float_as_int(f.w) * pitch;
                 if (one_cell) {
-                    const int key = ry * ncx + static_cast<int>(cxi[0] - ix0);
+                    const int key = ry + cxi[0];
                     if (key != last_key) {
                         float k00[CH], k10[CH], k01[CH], k11[CH];
 #pragma unroll
                         for (int c = 0; c < CH; ++c) {
-                            k00[c] = grid[c * CAP + key];
-                            k10[c] = grid[c * CAP + key + 1];
-                            k01[c] = grid[c * CAP + key + ncx];
-                            k11[c] = grid[c * CAP + key + ncx + 1];
+                            k00[c] = g[c * kGridCap + key];
+                            k10[c] = g[c * kGridCap + key + 1];
+                            k01[c] = g[c * kGridCap + key + pitch];
+                            k11[c] = g[c * kGridCap + key + pitch + 1];
                         }
                         cell.make(k00, k10, k01, k11);
                         last_key = key;
                     }
                     const auto row = cell.row(y, sy);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
+                    for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int key = ry * ncx + static_cast<int>(cxi[j] - ix0);
+                        const int key = ry + cxi[j];
                         float k00[CH], k10[CH], k01[CH], k11[CH];
 #pragma unroll
                         for (int c = 0; c < CH; ++c) {
-                            k00[c] = grid[c * CAP + key];
-                            k10[c] = grid[c * CAP + key + 1];
-                            k01[c] = grid[c * CAP + key + ncx];
-                            k11[c] = grid[c * CAP + key + ncx + 1];
+                            k00[c] = g[c * kGridCap + key];
+                            k10[c] = g[c * kGridCap + key + 1];
+                            k01[c] = g[c * kGridCap + key + pitch];
+                            k11[c] = g[c * kGridCap + key + pitch + 1];
                         }
                         Cell<KIND> cj;
                         cj.make(k00, k10, k01, k11);
                         acc[r][j] += Cell<KIND>::eval(cj.row(y, sy), x[j], sx[j], xs[j]);
                     }
                 }
-            } else {
-                // Cells too spread out for the shared grid (sub-pixel general
-                // octaves): hash the four corners per pixel.
+            }
+            continue;
+        }
+
+        // kModeDirect: corners hashed per pixel, coordinates per thread.
+        const float amp = od.amp;
+        if constexpr (kZg) {
+            if (od.cls == kClsFast && od.ppc == 1) {
+                ppc1_block(acc, [&](int r, float (&h)[5]) {
+#pragma unroll
+                    for (int q = 0; q < 5; ++q)
+                        corner_data<KIND>(base, tx0 + c0 + q, ty0 + r0 + r, amp, od.w, args.zero, &h[q]);
+                });
+                continue;
+            }
+        }
+        {
+            int64_t cxi[4];
+            float x[4], sx[4], xs[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                axis_coord(od, args.R, tx0 + c0 + j, &cxi[j], &x[j]);
+                sx[j] = smooth<ORDER>(x[j]);
+                xs[j] = x[j] * sx[j];
+            }
+#pragma unroll 1
+            for (int r = 0; r < 8; ++r) {
+                int64_t iy;
+                float y;
+                axis_coord(od, args.R, ty0 + r0 + r, &iy, &y);
+                const float sy = smooth<ORDER>(y);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     float k00[CH], k10[CH], k01[CH], k11[CH];
@@ -372,32 +661,36 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                     corner_data<KIND>(base, cxi[j] + 1, iy + 1, amp, od.w, args.zero, k11);
                     Cell<KIND> cj;
                     cj.make(k00, k10, k01, k11);
-                    acc[r][j] += Cell<KIND>::eval(cj.row(y, sy), x[j], sx[j], xs[j]);
+                    const float v = Cell<KIND>::eval(cj.row(y, sy), x[j], sx[j], xs[j]);
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr)
+                        if (rr == r) acc[rr][j] += v;
                 }
             }
         }
     }
 
     // ---- single fp32 store of the finished tile ----------------------------
-    float* base_out = out + static_cast<int64_t>(map) * args.map_stride;
-    const int64_t gx0 = tx0 + c0;
-    const int64_t lx0 = gx0 - args.ox;
-    const bool vec_ok = ((lx0 & 3) == 0) && ((args.ld & 3) == 0) &&
-                        ((reinterpret_cast<uintptr_t>(base_out) & 15) == 0) && lx0 >= 0 &&
+    const int64_t lx0 = tx0 + c0 - args.ox;
+    const int64_t ly0 = ty0 + r0 - args.oy;
+    float* row = out + static_cast<int64_t>(map) * args.map_stride + ly0 * args.ld + lx0;
+    const bool vec_ok = ((lx0 & 3) == 0) && ((args.ld & 3) == 0) && ((args.map_stride & 3) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && lx0 >= 0 &&
                         lx0 + 4 <= args.width;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-        const int64_t ly = ty0 + r0 + r - args.oy;
+    for (int r = 0; r < 8; ++r, row += args.ld) {
+        const int64_t ly = ly0 + r;
         if (ly < 0 || ly >= args.height) continue;
-        float* row = base_out + ly * args.ld;
+        const float v0 = acc[r][0] + racc[r], v1 = acc[r][1] + racc[r];
+        const float v2 = acc[r][2] + racc[r], v3 = acc[r][3] + racc[r];
         if (vec_ok) {
-            __stcs(reinterpret_cast<float4*>(row + lx0),
-                   make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+            *reinterpret_cast<float4*>(row) = make_float4(v0, v1, v2, v3);
         } else {
+            const float v[4] = {v0, v1, v2, v3};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int64_t lx = lx0 + j;
-                if (lx >= 0 && lx < args.width) row[lx] = acc[r][j];
+                if (lx >= 0 && lx < args.width) row[j] = v[j];
             }
         }
     }
@@ -405,10 +698,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 
 // ---- launch ------------------------------------------------------------------
 
-template <int KIND, int ORDER, int RPT>
+template <int KIND, int ORDER>
 static cudaError_t launch_t(const FbmArgs& a, float* out, cudaStream_t st) {
-    constexpr size_t smem = smem_bytes<KIND, RPT>();
-    auto kern = fbm2d_kernel<KIND, ORDER, RPT>;
+    constexpr size_t smem = smem_bytes<KIND>();
+    auto kern = fbm2d_kernel<KIND, ORDER>;
     static bool configured = false;  // benign race: idempotent attribute set
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -416,7 +709,7 @@ static cudaError_t launch_t(const FbmArgs& a, float* out, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    constexpr int TH = 8 * RPT;
+    constexpr int TH = kTH;
     const int64_t tiles_x = (a.ox + a.width - a.tile_x0 + kTW - 1) / kTW;
     const int64_t tiles_y = (a.oy + a.height - a.tile_y0 + TH - 1) / TH;
     dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
@@ -425,23 +718,22 @@ static cudaError_t launch_t(const FbmArgs& a, float* out, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-int fbm2d_tile_h() { return 64; }
+int fbm2d_tile_h() { return kTH; }
 
 cudaError_t fbm2d_launch(int kind, int order, const FbmArgs& a, float* out, cudaStream_t st) {
-    constexpr int RPT = 8;
     if (order == 5) {
         switch (kind) {
-            case kZgPaper: return launch_t<kZgPaper, 5, RPT>(a, out, st);
-            case kZgSeparable: return launch_t<kZgSeparable, 5, RPT>(a, out, st);
-            case kGeneric: return launch_t<kGeneric, 5, RPT>(a, out, st);
-            default: return launch_t<kPerlin, 5, RPT>(a, out, st);
+            case kZgPaper: return launch_t<kZgPaper, 5>(a, out, st);
+            case kZgSeparable: return launch_t<kZgSeparable, 5>(a, out, st);
+            case kGeneric: return launch_t<kGeneric, 5>(a, out, st);
+            default: return launch_t<kPerlin, 5>(a, out, st);
         }
     }
     switch (kind) {
-        case kZgPaper: return launch_t<kZgPaper, 3, RPT>(a, out, st);
-        case kZgSeparable: return launch_t<kZgSeparable, 3, RPT>(a, out, st);
-        case kGeneric: return launch_t<kGeneric, 3, RPT>(a, out, st);
-        default: return launch_t<kPerlin, 3, RPT>(a, out, st);
+        case kZgPaper: return launch_t<kZgPaper, 3>(a, out, st);
+        case kZgSeparable: return launch_t<kZgSeparable, 3>(a, out, st);
+        case kGeneric: return launch_t<kGeneric, 3>(a, out, st);
+        default: return launch_t<kPerlin, 3>(a, out, st);
     }
 }
 

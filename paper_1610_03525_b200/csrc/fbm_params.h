@@ -6,6 +6,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>
+
 namespace tg {
 
 // Per-octave sampling class, a function of the configuration only (never of
@@ -24,6 +26,24 @@ enum KernelKind : int32_t { kZgPaper = 0, kZgSeparable = 1, kGeneric = 2, kPerli
 constexpr int kMaxOctaves = 32;
 constexpr int kMaxBatch = 64;
 
+// 2D tile geometry and per-CTA shared-memory budget (fbm2d.cu).
+constexpr int kTileW = 128;        // 32 lanes x 4 columns
+constexpr int kTileH = 64;         // 8 warps x 8 rows
+constexpr int kGridCap = 12288;    // lattice-corner floats per channel per CTA
+constexpr int kTabSlots = 4;       // per-CTA sampling tables (general octaves)
+constexpr int kLutLog2Max = 13;    // device row LUT covers ppc = 1 .. 8192
+
+// Per-octave evaluation mode: a function of the configuration only (never of
+// the window), so every window reproduces the full-map bits.
+enum Mode : int32_t {
+    kModeSubInt = 0,  // samples on lattice points: v = h(ix, iy), one hash per pixel
+    kModePpc1 = 1,    // zg, 1 px per cell: v = 0.25*((h00+h10) + (h01+h11))
+    kModeBlock2 = 2,  // zg, 2 px per cell: 2 x 4 cells per thread block
+    kModeBlock = 3,   // power-of-two ppc >= 4: one cell per 4-column group
+    kModeGrid = 4,    // shared corner grid + per-CTA sampling tables
+    kModeDirect = 5,  // corners hashed per pixel (over the CTA budget)
+};
+
 struct OctDev {
     uint64_t oct_key;  // octave * K2 (lattice.hpp:47); seed term added per map
     double freq;       // f0 * ratio^i by repeated multiplication (fbm.hpp:155-158)
@@ -34,6 +54,14 @@ struct OctDev {
     int32_t ppc;       // pixels per cell (fast)
     int32_t shift;     // log2(ppc) when ppc is a power of two, else -1
     int64_t k;         // freq / R (sub-integer class)
+    // static per-CTA plan, computed on the host (capi.cu plan_octaves)
+    int32_t mode;      // Mode
+    int32_t ncx, ncy;  // corner grid shape (exact when aligned, upper bound otherwise)
+    int32_t pitch;     // grid row stride (floats, multiple of 4)
+    int32_t goff;      // grid offset (floats per channel, multiple of 4)
+    int32_t tslot;     // sampling-table slot (kModeGrid) or -1
+    int32_t lut_off;   // offset of this ppc's row LUT (aligned modes) or -1
+    int32_t pad;
 };
 
 struct FbmArgs {
@@ -47,6 +75,10 @@ struct FbmArgs {
     int32_t zero;            // ZeroSource
     int32_t n_maps;
     int32_t pad;
+    // Row LUT of the smoothstep order in use: for ppc = 2^k, entries
+    // lut[2^k - 1 + r] = (x, S(x), S(x) - x, x*S(x)) with x = (r + 0.5)/ppc
+    // (kernels2d.hpp:214-239 at phase 0.5), computed in fp64 and rounded.
+    const float4* lut;
     uint64_t seed_key[kMaxBatch];  // seed * K1 per map (lattice.hpp:47)
     OctDev oct[kMaxOctaves];
 };

@@ -4,10 +4,14 @@
 // peak used as the FP32 roofline denominator.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "../../include/polyterrain_b200.h"
+#include "fbm_params.h"
 #include "lattice.cuh"
 
 namespace tg {
@@ -40,6 +44,41 @@ cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uin
     lattice_kernel<<<static_cast<unsigned>(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, st>>>(
         what, keys, n, lane, out);
     return cudaGetLastError();
+}
+
+// Row LUTs (kernels2d::build_row_lut at phase 0.5, kernels2d.hpp:214-239) for
+// every power-of-two ppc up to 2^kLutLog2Max, both smoothstep orders, computed
+// once per device in fp64 and rounded to fp32: entry (x, S(x), S(x)-x, x*S(x)).
+// Immutable after creation, so concurrent callers share it (like the
+// reference's thread-local cached_row_lut, kernels2d.hpp:246-259).
+const float4* row_lut(int order) {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static float4* luts[kMaxDev][2] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    const int oi = order == 5 ? 1 : 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (luts[dev][oi]) return luts[dev][oi];
+    const int n = (1 << (kLutLog2Max + 1)) - 1;
+    std::vector<float4> h(static_cast<size_t>(n));
+    for (int k = 0; k <= kLutLog2Max; ++k) {
+        const int ppc = 1 << k;
+        for (int r = 0; r < ppc; ++r) {
+            const double x = (static_cast<double>(r) + 0.5) / static_cast<double>(ppc);
+            const double sv = order == 5 ? x * x * x * (10.0 + x * (6.0 * x - 15.0)) : x * x * (3.0 - 2.0 * x);
+            h[static_cast<size_t>(ppc - 1 + r)] = make_float4(static_cast<float>(x), static_cast<float>(sv),
+                                                              static_cast<float>(sv - x), static_cast<float>(x * sv));
+        }
+    }
+    float4* d = nullptr;
+    if (cudaMalloc(&d, sizeof(float4) * n) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h.data(), sizeof(float4) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    luts[dev][oi] = d;
+    return d;
 }
 
 __global__ void widen_kernel(const float* __restrict__ in, double* __restrict__ out, uint64_t n) {

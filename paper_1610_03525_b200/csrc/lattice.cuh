@@ -20,28 +20,36 @@ constexpr uint64_t kIzMul = 0xA24BAED4963EE407ULL;    // 3D extension (TG_PACK_K
 constexpr uint64_t kAngleLane = 0xA0761D6478BD642FULL;      // lattice.hpp:53
 constexpr uint64_t kMagnitudeLane = 0xE7037ED1A0B428DBULL;  // lattice.hpp:54
 
-// lattice.hpp:35-42.  Written on 32-bit halves so the SASS is exactly the
-// minimal sequence: z ^= z >> 33 only touches the low word
-// (lo ^= hi >> 1); each 64x64->64 multiply is one IMAD.WIDE.U32 plus two
-// IMAD for the cross terms.
+// z *= M (mod 2^64) on 32-bit halves in exactly three IMADs: the wide
+// product of the low words, then both cross terms accumulated into its high
+// word.  Inline PTX keeps ptxas from re-associating into four instructions.
+#define TG_MUL64(lo, hi, ML, MH)                                                     \
+    do {                                                                             \
+        uint32_t plo_, phi_;                                                         \
+        asm("{\n\t.reg .b64 p;\n\tmul.wide.u32 p, %2, " #ML ";\n\t"                 \
+            "mov.b64 {%0, %1}, p;\n\tmad.lo.u32 %1, %3, " #ML ", %1;\n\t"           \
+            "mad.lo.u32 %1, %2, " #MH ", %1;\n\t}"                                  \
+            : "=r"(plo_), "=r"(phi_)                                                 \
+            : "r"(lo), "r"(hi));                                                     \
+        lo = plo_;                                                                   \
+        hi = phi_;                                                                   \
+    } while (0)
+
+// lattice.hpp:35-42 (murmur3 fmix64) up to, but excluding, the final
+// xorshift: z ^= z >> 33 only touches the low word (lo ^= hi >> 1).
+__device__ __forceinline__ void mix64_pre(uint64_t z, uint32_t& lo, uint32_t& hi) {
+    lo = static_cast<uint32_t>(z);
+    hi = static_cast<uint32_t>(z >> 32);
+    lo ^= hi >> 1;
+    TG_MUL64(lo, hi, 0xED558CCD, 0xFF51AFD7);
+    lo ^= hi >> 1;
+    TG_MUL64(lo, hi, 0x1A85EC53, 0xC4CEB9FE);
+}
+
+// lattice.hpp:35-42 — the full 64-bit finalizer.
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
-    lo ^= hi >> 1;
-    {
-        const uint32_t ml = 0xED558CCDu, mh = 0xFF51AFD7u;
-        const uint64_t p = static_cast<uint64_t>(lo) * ml;
-        const uint32_t nh = static_cast<uint32_t>(p >> 32) + lo * mh + hi * ml;
-        lo = static_cast<uint32_t>(p);
-        hi = nh;
-    }
-    lo ^= hi >> 1;
-    {
-        const uint32_t ml = 0x1A85EC53u, mh = 0xC4CEB9FEu;
-        const uint64_t p = static_cast<uint64_t>(lo) * ml;
-        const uint32_t nh = static_cast<uint32_t>(p >> 32) + lo * mh + hi * ml;
-        lo = static_cast<uint32_t>(p);
-        hi = nh;
-    }
+    uint32_t lo, hi;
+    mix64_pre(z, lo, hi);
     lo ^= hi >> 1;
     return (static_cast<uint64_t>(hi) << 32) | lo;
 }
@@ -51,6 +59,24 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // wrap two's-complement exactly like the reference's static_cast<uint64_t>.
 __device__ __forceinline__ uint64_t pack_xy(uint64_t base, int64_t ix, int64_t iy) {
     return base + static_cast<uint64_t>(ix) * kIxMul + static_cast<uint64_t>(iy) * kIyMul;
+}
+
+// corner_height scaled by 2^63 as an exact-rounding float:
+//   corner_height = (z >> 11)*2^-52 - 1 = t*2^-52,  t = (int64)(z ^ 2^63) >> 11,
+// and RN(t * 2^11) = RN(t) * 2^11, so converting (z ^ 2^63) with its low 11
+// bits cleared rounds the exact reference value once.  The caller multiplies
+// by amp * 2^-63 (a power-of-two rescale, exact).  The clear folds into the
+// final xorshift: one LOP3 computes (lo ^ (hi >> 1)) & ~0x7ff.
+__device__ __forceinline__ float height_scaled_from_pre(uint32_t lo, uint32_t hi) {
+    const uint32_t l = (lo ^ (hi >> 1)) & 0xFFFFF800u;
+    const uint32_t h = hi ^ 0x80000000u;
+    return __ll2float_rn(static_cast<long long>((static_cast<uint64_t>(h) << 32) | l));
+}
+
+__device__ __forceinline__ float height_scaled(uint64_t packed) {
+    uint32_t lo, hi;
+    mix64_pre(packed, lo, hi);
+    return height_scaled_from_pre(lo, hi);
 }
 
 // float(corner_height) with one round-to-nearest (lattice.hpp:56-64).
@@ -67,7 +93,7 @@ __device__ __forceinline__ float unit_from_hash(uint64_t z) {
 }
 
 __device__ __forceinline__ float corner_height(uint64_t base, int64_t ix, int64_t iy) {
-    return height_from_hash(mix64(pack_xy(base, ix, iy)));
+    return height_scaled(pack_xy(base, ix, iy)) * 0x1p-63f;
 }
 
 // corner_unit_gradient (lattice.hpp:80-83): angle = unit * 2*pi, so

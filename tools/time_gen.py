@@ -1,0 +1,47 @@
+"""Quick device timing of generation launches (CUDA events, rotating outputs).
+
+    python tools/time_gen.py [--configs cfg1,cfg2,cfg3p,cfg5] [--iters 50]
+Prints one line per config: mean us per launch and G sample-octaves/s.
+Set TG_LIB_PATH to time a library variant.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1610_03525_b200 as pt  # noqa: E402
+
+CONFIGS = {
+    "cfg1": (dict(seed=1, resolution=1024, base_frequency=8, octaves=8), 1024, 1024),
+    "cfg2": (dict(seed=1, smoothstep=5, resolution=4096, base_frequency=8, octaves=12), 4096, 4096),
+    "cfg2sep": (dict(seed=1, method=pt.Method.zg_separable, smoothstep=5, resolution=4096, base_frequency=8,
+                     octaves=12), 4096, 4096),
+    "cfg3p": (dict(seed=1, method=pt.Method.perlin3, resolution=4096, base_frequency=8, octaves=12), 4096, 4096),
+    "cfg3p5": (dict(seed=1, method=pt.Method.perlin5, resolution=4096, base_frequency=8, octaves=12), 4096, 4096),
+    "cfg3g": (dict(seed=1, method=pt.Method.generic, resolution=4096, base_frequency=8, octaves=12), 4096, 4096),
+    "cfg5": (dict(seed=1, smoothstep=5, resolution=32768, base_frequency=32, octaves=16), 4096, 4096),
+}
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="cfg1,cfg2,cfg3p,cfg5")
+ap.add_argument("--iters", type=int, default=50)
+a = ap.parse_args()
+for name in a.configs.split(","):
+    kw, w, h = CONFIGS[name]
+    cfg = pt.FbmConfig(**kw)
+    bufs = [torch.empty((h, w), dtype=torch.float32, device="cuda") for _ in range(3)]
+    for i in range(5):
+        pt.generate_rect_device(cfg, (0, 0), w, h, bufs[i % 3])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(a.iters):
+        pt.generate_rect_device(cfg, (0, 0), w, h, bufs[i % 3])
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / a.iters
+    so = w * h * cfg.octaves
+    print(f"{name:8s} {us:9.1f} us  {so / us / 1e3:8.1f} G sample-oct/s  ({w}x{h}x{cfg.octaves})", flush=True)
