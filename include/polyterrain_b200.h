@@ -182,6 +182,17 @@ int tg_coastline_mask(const float* dev_map, int64_t resolution, double sea_level
 int tg_coastline_boxcount(const float* dev_map, int64_t resolution, double sea_level,
                           const int32_t* sizes, int32_t n_sizes, int64_t* out_counts,
                           int64_t* out_coast_pixels, int64_t* out_land_count, void* stream);
+/* Row-band form for sharded terrains: `rows` rows of `width` (pitch ld)
+ * starting at dev_rows; when has_top / has_bottom the rows just above / below
+ * are present in memory (regenerated halos), otherwise the band touches the
+ * map edge.  Boxes are anchored at the band's first row, so band starts must
+ * be multiples of every box size for the per-band counts to sum to the
+ * whole-map counts.  Counts only; the all-land/water checks are the caller's
+ * (they are global properties).  Synchronous. */
+int tg_coastline_boxcount_band(const float* dev_rows, int64_t width, int64_t rows, int64_t ld,
+                               int32_t has_top, int32_t has_bottom, double sea_level,
+                               const int32_t* sizes, int32_t n_sizes, int64_t* out_counts,
+                               int64_t* out_coast_pixels, int64_t* out_land_count, void* stream);
 /* Box counts of an explicit u8 mask (box_count on a CoastlineMask). */
 int tg_boxcount_mask(const uint8_t* dev_mask, int64_t resolution, const int32_t* sizes,
                      int32_t n_sizes, int64_t* out_counts, void* stream);
@@ -192,6 +203,20 @@ int tg_boxcount_mask(const uint8_t* dev_mask, int64_t resolution, const int32_t*
 int tg_variogram_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld,
                      const int32_t* lags, int32_t n_lags, double* out_sum_sq,
                      int64_t* out_pairs, void* stream);
+
+/* Band form: only pairs whose first point lies in the first `pair_rows` rows
+ * (the rows below are lookahead regenerated for a row-band shard), so the
+ * per-shard sums add up to the whole-map variogram. */
+int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld,
+                          int64_t pair_rows, const int32_t* lags, int32_t n_lags,
+                          double* out_sum_sq, int64_t* out_pairs, void* stream);
+/* Local radix-select histogram (2^bits bins of key digit (shift, bits) among
+ * keys with (key & mask) == prefix; key = order-preserving u32 of the fp32
+ * value) over a strided window, to host.  The per-rank step of a distributed
+ * upper median: ranks sum their histograms (NCCL all-reduce) and pick. */
+int tg_histogram_f32(const float* dev_rows, int64_t width, int64_t rows, int64_t ld,
+                     uint32_t prefix, uint32_t mask, int32_t shift, int32_t bits,
+                     uint64_t* out_hist, void* stream);
 
 /* ---- measurement helpers ---------------------------------------------------- */
 

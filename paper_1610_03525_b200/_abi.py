@@ -103,7 +103,11 @@ SIGNATURES = {
     "tg_median_f32": (C.c_int, [P, U64, C.POINTER(C.c_float), P]),
     "tg_coastline_mask": (C.c_int, [P, I64, F64, P, C.POINTER(I64), P]),
     "tg_coastline_boxcount": (C.c_int, [P, I64, F64, P, I32, P, C.POINTER(I64), C.POINTER(I64), P]),
+    "tg_coastline_boxcount_band": (C.c_int, [P, I64, I64, I64, I32, I32, F64, P, I32, P, C.POINTER(I64),
+                                             C.POINTER(I64), P]),
     "tg_boxcount_mask": (C.c_int, [P, I64, P, I32, P, P]),
+    "tg_variogram_band_f32": (C.c_int, [P, I64, I64, I64, I64, P, I32, P, P, P]),
+    "tg_histogram_f32": (C.c_int, [P, I64, I64, I64, C.c_uint32, C.c_uint32, I32, I32, P, P]),
     "tg_variogram_f32": (C.c_int, [P, I64, I64, I64, P, I32, P, P, P]),
     "tg_measure_ffma_peak": (C.c_int, [C.POINTER(F64), C.POINTER(F64)]),
 }

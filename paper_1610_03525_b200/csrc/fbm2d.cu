@@ -414,8 +414,8 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, height_scaled(X[j] + Y), acc[r][j]);
-                Y += dY;
+                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, height_scaled(add64(X[j], Y)), acc[r][j]);
+                Y = add64(Y, dY);
             }
             continue;
         }

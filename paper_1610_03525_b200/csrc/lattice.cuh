@@ -54,6 +54,14 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
+// 64-bit add kept as IADD3 + IADD3.X (stops ptxas from re-deriving per-pixel
+// keys with extra wide multiplies).
+__device__ __forceinline__ uint64_t add64(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.u64 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // lattice.hpp:46-50 split as pack = base + ix*K3 + iy*K4 with
 // base = seed*K1 + octave*K2 hoisted per octave.  ix/iy are signed 64-bit and
 // wrap two's-complement exactly like the reference's static_cast<uint64_t>.
@@ -69,8 +77,13 @@ __device__ __forceinline__ uint64_t pack_xy(uint64_t base, int64_t ix, int64_t i
 // final xorshift: one LOP3 computes (lo ^ (hi >> 1)) & ~0x7ff.
 __device__ __forceinline__ float height_scaled_from_pre(uint32_t lo, uint32_t hi) {
     const uint32_t l = (lo ^ (hi >> 1)) & 0xFFFFF800u;
-    const uint32_t h = hi ^ 0x80000000u;
-    return __ll2float_rn(static_cast<long long>((static_cast<uint64_t>(h) << 32) | l));
+    float f;
+    // one LOP3 for the sign flip of the high word, then s64 -> f32 (RN)
+    asm("{\n\t.reg .b32 h;\n\t.reg .b64 v;\n\txor.b32 h, %2, 0x80000000;\n\t"
+        "mov.b64 v, {%1, h};\n\tcvt.rn.f32.s64 %0, v;\n\t}"
+        : "=f"(f)
+        : "r"(l), "r"(hi));
+    return f;
 }
 
 __device__ __forceinline__ float height_scaled(uint64_t packed) {

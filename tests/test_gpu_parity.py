@@ -367,3 +367,34 @@ def test_fbm3d_subvolume_bit_exact():
     sub = torch.empty((32, 64, 96), dtype=torch.float32, device="cuda")
     pt.generate3d_device(cfg, (32, 64, 96), (32, 64, 96), sub)
     assert torch.equal(sub, full[96:128, 64:128, 32:128])
+
+
+# ---- row-band shards (multi-GPU unit) -----------------------------------
+
+def test_device_band_stats_sum_to_whole_map(oracle):
+    from paper_1610_03525_b200.shard import Comm, DeviceBackend, plan_band, terrain_stats
+
+    cfgp = pt.FbmConfig(method=0, smoothstep=5, seed=3, resolution=1024, base_frequency=4, octaves=12)
+    sizes, lags = [2, 4, 8, 16, 32, 64], [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
+    whole = terrain_stats(plan_band(1024, 1024, 1, 0, align=256, max_lag=512), DeviceBackend(cfgp), Comm(),
+                          sizes, lags)
+    # the whole-map numbers against the oracle on the GPU's own map
+    m = gen(cfgp.to_c(), 0, 0, 1024).cpu().numpy().astype(np.float64)
+    sea = oracle.upper_median(m)
+    assert whole.sea_level == sea
+    st, mask, land = oracle.coastline_mask(m, sea)
+    st, counts, d, k, r2 = oracle.box_count(mask, sizes)
+    assert whole.counts == list(counts) and whole.coast_pixels == int(mask.sum())
+    ss, pr = oracle.variogram(m, lags)
+    assert np.array_equal(whole.pairs, pr) and np.allclose(whole.sum_sq, ss, rtol=1e-10)
+    # 4 bands evaluated one after another on this GPU, summed on the host
+    tot_c, tot_ss, tot_pr, tot_coast = np.zeros(len(sizes), np.int64), 0.0, 0, 0
+    for r in range(4):
+        b = plan_band(1024, 1024, 4, r, align=256, max_lag=512)
+        s = terrain_stats(b, DeviceBackend(cfgp), Comm(), sizes, lags, sea_level=sea)
+        tot_c += np.array(s.counts)
+        tot_ss = tot_ss + s.sum_sq
+        tot_pr = tot_pr + s.pairs
+        tot_coast += s.coast_pixels
+    assert list(tot_c) == whole.counts and tot_coast == whole.coast_pixels
+    assert np.array_equal(tot_pr, whole.pairs) and np.allclose(tot_ss, whole.sum_sq, rtol=1e-10)
