@@ -124,7 +124,9 @@ int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_
                         float* dev_out, uint64_t n_out, void* stream);
 /* Rectangular window with a row pitch (elements); used for row bands and
  * chunk grids.  Same per-pixel values as the square form (pure function of
- * the global pixel). */
+ * the global pixel).  Unlike the square form (fbm.hpp:551-558) the origin
+ * need not sit on an octave-0 cell boundary, so shards can regenerate halo
+ * rows; |origin| <= 2^40 still applies. */
 int tg_fbm_generate_rect_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
                              int64_t height, float* dev_out, int64_t ld, void* stream);
 /* A batch of maps that differ only in seed: out[b] is the window for

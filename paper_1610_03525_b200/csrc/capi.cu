@@ -208,7 +208,7 @@ int validate_cfg(const tg_fbm_config* c) {
 }
 
 int validate_window(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width,
-                    int64_t height) {
+                    int64_t height, bool require_alignment = true) {
     if (width < 1 || width > TG_MAX_EXTENT || height < 1 || height > TG_MAX_EXTENT)
         return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
     const int64_t origin[2] = {ox, oy};
@@ -216,7 +216,7 @@ int validate_window(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t widt
         if (o < -(1LL << 40) || o > (1LL << 40))
             return fail(TG_EVALIDATION, "generate: origin out of supported range");
         const int64_t prod = o * c->base_frequency;
-        if (((prod % c->resolution) + c->resolution) % c->resolution != 0)
+        if (require_alignment && ((prod % c->resolution) + c->resolution) % c->resolution != 0)
             return fail(TG_EVALIDATION, "generate: origin must be aligned to octave-0 cell boundaries");
     }
     return TG_OK;
@@ -293,7 +293,9 @@ int tg_device_count(void) {
 int tg_fbm_generate_rect_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
                              int64_t height, float* dev_out, int64_t ld, void* stream) {
     if (int st = validate_cfg(cfg)) return st;
-    if (int st = validate_window(cfg, ox, oy, width, height)) return st;
+    // The chunk/band primitive accepts any origin: every value is a pure
+    // function of (cfg, global pixel), so halo rows can be regenerated.
+    if (int st = validate_window(cfg, ox, oy, width, height, false)) return st;
     if (!dev_out) return fail(TG_EVALIDATION, "generate: null output");
     if (ld < width) return fail(TG_EVALIDATION, "generate: row pitch smaller than width");
     if (int st = device_ready()) return st;
@@ -311,6 +313,7 @@ int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_
         return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
     if (n_out != static_cast<uint64_t>(extent) * static_cast<uint64_t>(extent))
         return fail(TG_EVALIDATION, "generate: output buffer size mismatch");  // fbm.hpp:549
+    if (int st = validate_window(cfg, ox, oy, extent, extent)) return st;  // fbm.hpp:551-558
     return tg_fbm_generate_rect_f32(cfg, ox, oy, extent, extent, dev_out, extent, stream);
 }
 
