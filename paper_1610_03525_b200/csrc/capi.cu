@@ -106,8 +106,9 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
         std::memset(&d, 0, sizeof(d));
         d.oct_key = static_cast<uint64_t>(static_cast<uint32_t>(o)) * tg::kOctMul;
         d.freq = os.freq;
-        d.amp = static_cast<float>(os.amp);
-        d.w = static_cast<float>(w);
+        // ZeroSource (fbm.hpp:125-133): every corner datum 0 <=> amp = w = 0
+        d.amp = c->zero_lattice ? 0.0f : static_cast<float>(os.amp);
+        d.w = c->zero_lattice ? 0.0f : static_cast<float>(w);
         d.shift = -1;
         d.tslot = -1;
         d.lut_off = -1;
@@ -252,6 +253,22 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     const int64_t cand[4] = {ox - 256, ox + width + 256, oy - 256, oy + height + 256};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
     plan_octaves(c, gmax, a->oct, true);
+    // mode-homogeneous octave lists (fbm_params.h OctGroup)
+    const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
+    for (int o = 0; o < c->octaves; ++o) {
+        const tg::OctDev& d = a->oct[o];
+        auto push = [&](int g) { a->group[g][a->ngroup[g]++] = static_cast<int8_t>(o); };
+        const bool has_grid = d.mode == tg::kModePpc1 || d.mode == tg::kModeBlock2 || d.mode == tg::kModeBlock ||
+                              d.mode == tg::kModeGrid;
+        if (has_grid) push(d.lut_off >= 0 && d.mode != tg::kModeGrid && d.ncx * d.ncy <= 32 ? tg::kGProCoarse
+                                                                                            : tg::kGProFine);
+        if (d.mode == tg::kModeSubInt) push(tg::kGSub);
+        else if (zg && d.mode == tg::kModeBlock && d.shift >= 3) push(tg::kGBlk8);
+        else if (zg && d.mode == tg::kModeBlock && d.shift == 2) push(tg::kGBlk4);
+        else if (zg && d.mode == tg::kModeBlock2) push(tg::kGBlk2);
+        else if (zg && d.mode == tg::kModePpc1) push(tg::kGPpc1);
+        else push(tg::kGGen);
+    }
     a->lut = tg::row_lut(order_of(c));
     if (!a->lut) return fail(TG_EDEVICE, "row LUT allocation failed");
     return TG_OK;

@@ -3,22 +3,23 @@
 // Replaces the octave loop of generate_into_with_source
 // (terrain/fbm.hpp:541-628) and its render paths render_zg_fast (231-312),
 // render_generic_fast (321-379), render_perlin_fast (384-455) and
-// render_general (460-527).  One CTA owns a 128 x TH pixel tile whose
+// render_general (460-527).  One CTA owns a 128 x 64 pixel tile whose
 // accumulators stay in registers across ALL octaves; the map is written once
 // (4 B/pixel) instead of the reference's read-modify-write of a double buffer
 // per octave (fbm.hpp:187,193).
 //
-// The CTA runs one prologue for ALL octaves — sampling tables (cell index,
-// x, S(x)) and every octave's unique lattice corners hashed once into shared
-// memory — then a barrier-free octave loop in which each thread evaluates its
-// 4 x 8 pixels from the shared corners, with the cell polynomial factorised
-// per (cell, row):
+// The CTA runs one prologue for ALL octaves — every octave's unique lattice
+// corners for the tile hashed once into shared memory (plus per-CTA sampling
+// tables for general octaves) — then barrier-free loops over host-built,
+// mode-homogeneous octave lists in which each thread evaluates its 4 x 8
+// pixels from the shared corners with the cell polynomial factorised per
+// (cell, row):
 //   zg paper     v = c0 + sx*c1 + x*c2      (kernels2d.hpp:62-76)
 //   zg separable v = c0 + sx*c1
 //   perlin       v = a0 + x*a1 + sx*a2 + x*sx*a3   (kernels2d.hpp:163-173)
 //   generic      v = ((r3*x + r2)*x + r1)*x + r0    (kernels2d.hpp:124-134)
 // Octaves whose samples sit exactly on lattice points (kClsSubInt) need no
-// tables: each pixel hashes its one corner in registers.
+// grid: each pixel hashes its one corner in registers.
 //
 // Every pixel's arithmetic is a function of (config, global pixel) only, so
 // any window / tile decomposition reproduces the same bits (fbm.hpp:7-8).
@@ -30,7 +31,8 @@
 namespace tg {
 
 constexpr int kThreads = 256;
-constexpr int kTW = 128;  // 32 lanes x 4 columns
+constexpr int kTW = kTileW;
+constexpr int kTH = kTileH;
 
 template <int ORDER>
 __device__ __forceinline__ float smooth(float t) {
@@ -45,17 +47,12 @@ template <> struct Traits<kPerlin> { static constexpr int kCh = 2; };
 template <> struct Traits<kGeneric> { static constexpr int kCh = 3; };
 
 // Corner data of one lattice point from its packed key (lattice.hpp:46-50),
-// already scaled like the reference's render paths: zg/generic heights x amp
+// scaled like the reference's render paths: zg/generic heights x amp
 // (fbm.hpp:270,349), Perlin unit gradients x amp (409-420), generic gradients
-// unscaled (348).  amp63 = amp * 2^-63 (see height_scaled_from_pre).
+// x w, unscaled by amp (348).  amp63 = amp * 2^-63 (height_scaled_from_pre).
+// ZeroSource (fbm.hpp:125-133) is amp = w = 0, set by the host planner.
 template <int KIND>
-__device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float amp63, float w,
-                                                   int zero, float* d) {
-    if (zero) {
-#pragma unroll
-        for (int c = 0; c < Traits<KIND>::kCh; ++c) d[c] = 0.f;
-        return;
-    }
+__device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float amp63, float w, float* d) {
     if constexpr (KIND == kZgPaper || KIND == kZgSeparable) {
         d[0] = amp63 * height_scaled(p);
     } else if constexpr (KIND == kPerlin) {
@@ -74,9 +71,9 @@ __device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float 
 }
 
 template <int KIND>
-__device__ __forceinline__ void corner_data(uint64_t base, int64_t ix, int64_t iy, float amp,
-                                            float w, int zero, float* d) {
-    corner_data_packed<KIND>(pack_xy(base, ix, iy), amp, amp * 0x1p-63f, w, zero, d);
+__device__ __forceinline__ void corner_data(uint64_t base, int64_t ix, int64_t iy, float amp, float w,
+                                            float* d) {
+    corner_data_packed<KIND>(pack_xy(base, ix, iy), amp, amp * 0x1p-63f, w, d);
 }
 
 // Per-cell constants (from the 4 corners) and per-(cell,row) coefficients.
@@ -207,8 +204,6 @@ __device__ __forceinline__ void axis_coord(const OctDev& od, double R, int64_t g
     }
 }
 
-constexpr int kTH = kTileH;
-
 struct TabSlot {
     float colX[kTW], colS[kTW], colXS[kTW];
     int32_t colI[kTW];  // cell index relative to the tile's first cell
@@ -220,11 +215,12 @@ constexpr size_t smem_bytes() {
     return sizeof(TabSlot) * kTabSlots + sizeof(float) * Traits<KIND>::kCh * kGridCap;
 }
 
-// 0.25*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
+// q*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
 // rows r = 0..8 of a 5-wide corner strip: x = y = 0.5 makes every zero-
-// gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners.
+// gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners
+// (q = amp/4, folded with the grid's 2^-63 height scale).
 template <class Fetch>
-__device__ __forceinline__ void ppc1_block(float (&acc)[8][4], Fetch fetch) {
+__device__ __forceinline__ void ppc1_block(float (&acc)[8][4], float q, Fetch fetch) {
     float h[5];
     fetch(0, h);
     float hs[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
@@ -234,16 +230,42 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[8][4], Fetch fetch) {
         const float ns[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            acc[r][j] = fmaf(0.25f, hs[j] + ns[j], acc[r][j]);
+            acc[r][j] = fmaf(q, hs[j] + ns[j], acc[r][j]);
             hs[j] = ns[j];
         }
     }
 }
 
-template <int KIND, int ORDER>
+// zero-gradient cell rows r_begin.. of one cell: c0 = h00 + sy*dy goes into
+// the per-row accumulator (common to the 4 columns), the rest per pixel.
+template <int KIND, int NR>
+__device__ __forceinline__ void zg_rows(float (&acc)[8][4], float (&racc)[8], int r_begin,
+                                        const float4* __restrict__ Ly, const float (&x)[4],
+                                        const float (&sx)[4], float h00, float h10, float h01,
+                                        float h11) {
+    const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+        const int r = r_begin + rr;
+        const float4 f = Ly[rr];
+        racc[r] += fmaf(f.y, dy, h00);
+        if constexpr (KIND == kZgPaper) {
+            const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j]));
+        } else {
+            const float c1 = fmaf(a, f.y, dx);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(sx[j], c1, acc[r][j]);
+        }
+    }
+}
+
 #ifndef TG_ZG_MIN_BLOCKS
 #define TG_ZG_MIN_BLOCKS 3
 #endif
+
+template <int KIND, int ORDER>
 __global__ void __launch_bounds__(kThreads, (KIND == kZgPaper || KIND == kZgSeparable) ? TG_ZG_MIN_BLOCKS : 1)
 fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     constexpr int CH = Traits<KIND>::kCh;
@@ -257,34 +279,34 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     const int warp = tid >> 5;
     const int64_t tx0 = args.tile_x0 + static_cast<int64_t>(blockIdx.x) * kTW;
     const int64_t ty0 = args.tile_y0 + static_cast<int64_t>(blockIdx.y) * kTH;
-    const int map = blockIdx.z;
-    const uint64_t seed_key = args.seed_key[map];
+    const uint64_t seed_key = args.seed_key[blockIdx.z];
     const int c0 = lane * 4;
     const int r0 = warp * 8;
-    const int nocts = args.octaves;
+
+    // Grid contents: zero-gradient grids hold raw height_scaled() values (the
+    // octave amplitude is folded in at evaluation); Perlin/generic grids hold
+    // amplitude-scaled corner data.
+    auto grid_value = [&](uint64_t p, const OctDev& od, float* d) {
+        if constexpr (kZg) d[0] = height_scaled(p);
+        else corner_data_packed<KIND>(p, od.amp, od.amp * 0x1p-63f, od.w, d);
+    };
 
     // ---- prologue: every octave's tile corners (and, for general octaves,
     // sampling tables) into shared memory; one barrier for the whole kernel.
-    // Coarse aligned octaves (<= 32 corners per tile) first: one warp per
-    // octave, one corner per lane.
-    for (int o = warp; o < nocts; o += kThreads / 32) {
-        const OctDev& od = args.oct[o];
-        if (od.mode == kModeSubInt || od.mode == kModeDirect || od.lut_off < 0 || od.ncx * od.ncy > 32)
-            continue;
+    // (a) coarse aligned octaves (<= 32 corners): one warp per octave.
+    for (int q = warp; q < args.ngroup[kGProCoarse]; q += kThreads / 32) {
+        const OctDev& od = args.oct[args.group[kGProCoarse][q]];
         if (lane < od.ncx * od.ncy) {
             const int cy = lane / od.ncx, cx = lane - cy * od.ncx;
-            const uint64_t p = pack_xy(seed_key + od.oct_key, (tx0 >> od.shift) + cx, (ty0 >> od.shift) + cy);
             float d[CH];
-            corner_data_packed<KIND>(p, od.amp, od.amp * 0x1p-63f, od.w, args.zero, d);
+            grid_value(pack_xy(seed_key + od.oct_key, (tx0 >> od.shift) + cx, (ty0 >> od.shift) + cy), od, d);
 #pragma unroll
             for (int c = 0; c < CH; ++c) grid[c * kGridCap + od.goff + cy * od.pitch + cx] = d[c];
         }
     }
-    for (int o = 0; o < nocts; ++o) {
-        const OctDev& od = args.oct[o];
-        const int mode = od.mode;
-        if (mode == kModeSubInt || mode == kModeDirect) continue;
-        if (od.lut_off >= 0 && od.ncx * od.ncy <= 32 && mode != kModeGrid) continue;  // done above
+    // (b) everything else with a grid
+    for (int q = 0; q < args.ngroup[kGProFine]; ++q) {
+        const OctDev& od = args.oct[args.group[kGProFine][q]];
         const uint64_t base = seed_key + od.oct_key;
         const bool aligned = od.lut_off >= 0;  // power-of-two ppc on the aligned tile grid
         int64_t ix0, iy0;
@@ -302,7 +324,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             ncx = static_cast<int>(ixe - ix0 + 2);  // <= the planned bound
             ncy = static_cast<int>(iye - iy0 + 2);
         }
-        if (mode == kModeGrid) {
+        if (od.mode == kModeGrid) {
             TabSlot& tb = tabs[od.tslot];
             if (tid < kTW) {
                 int64_t i;
@@ -324,37 +346,32 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
         }
         const int pitch = od.pitch;
         const uint64_t p0 = pack_xy(base, ix0, iy0);
-        const float amp = od.amp, amp63 = od.amp * 0x1p-63f, w = od.w;
         float* g = grid + od.goff;
-        if (CH == 1 && aligned && od.shift <= 4) {
+        if (kZg && aligned && od.shift <= 4) {
             // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc.  The main
             // block goes 4 consecutive corners per lane (four independent hash
             // chains, keys advanced by +K3, one 16-byte store); the last column
             // and row go through the flat loop.
             const int sh = od.shift;
             const int Wm = kTW >> sh, Hm = kTH >> sh;
-            const int lsh = 5 - sh;            // log2(lanes per corner row) = log2(Wm / 4)
+            const int lsh = 5 - sh;  // log2(lanes per corner row) = log2(Wm / 4)
             const int cg = lane & ((1 << lsh) - 1), rs = lane >> lsh;
             const int rstep = (kThreads / 32) << sh;  // rows per pass over all warps
             const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
             for (int cy = (warp << sh) + rs; cy < Hm; cy += rstep) {
                 const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
                 float4 v;
-                v.x = amp63 * height_scaled(p);
-                v.y = amp63 * height_scaled(p + kIxMul);
-                v.z = amp63 * height_scaled(p + 2 * kIxMul);
-                v.w = amp63 * height_scaled(p + 3 * kIxMul);
-                if (args.zero) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                v.x = height_scaled(p);
+                v.y = height_scaled(add64(p, kIxMul));
+                v.z = height_scaled(add64(p, 2 * kIxMul));
+                v.w = height_scaled(add64(p, 3 * kIxMul));
                 *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = v;
             }
             for (int i = tid; i < Hm + 1 + Wm; i += kThreads) {
                 const int cx = i <= Hm ? Wm : i - Hm - 1;
                 const int cy = i <= Hm ? i : Hm;
-                const uint64_t p = p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
-                                   static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
-                float d[CH];
-                corner_data_packed<KIND>(p, amp, amp63, w, args.zero, d);
-                g[cy * pitch + cx] = d[0];
+                g[cy * pitch + cx] = height_scaled(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                                                   static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul);
             }
         } else {
             // Any other shape: flat corner list, four hash chains per thread.
@@ -369,9 +386,9 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                     const int cy = static_cast<int>((static_cast<float>(i) + 0.5f) * rcp);
                     const int cx = i - cy * ncx;
                     dst[u] = cy * pitch + cx;
-                    const uint64_t p = p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
-                                       static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
-                    corner_data_packed<KIND>(p, amp, amp63, w, args.zero, d[u]);
+                    grid_value(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                                   static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul,
+                               od, d[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -384,9 +401,9 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     }
     __syncthreads();
 
-    // ---- per-octave evaluation of the thread's 4 x 8 pixels (no barriers) ---
+    // ---- evaluation of the thread's 4 x 8 pixels (no barriers) --------------
     float acc[8][4];
-    float racc[8];  // per-row terms common to the 4 columns (zg block mode)
+    float racc[8];  // per-row terms common to the 4 columns (zg block modes)
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         racc[r] = 0.f;
@@ -394,22 +411,105 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
         for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
     }
 
-    for (int o = 0; o < nocts; ++o) {
-        const OctDev& od = args.oct[o];
-        const int mode = od.mode;
-        const uint64_t base = seed_key + od.oct_key;
+    if constexpr (kZg) {
+        // power-of-two ppc >= 8: the 4 x 8 block lies in one cell
+        for (int q = 0; q < args.ngroup[kGBlk8]; ++q) {
+            const OctDev& od = args.oct[args.group[kGBlk8][q]];
+            const int sh = od.shift, mask = od.ppc - 1;
+            const float4* L = args.lut + od.lut_off;
+            const int xo = static_cast<int>(tx0 & mask) + c0;
+            const int yo = static_cast<int>(ty0 & mask) + r0;
+            const float* g = grid + od.goff + (yo >> sh) * od.pitch + (xo >> sh);
+            const float amp = od.amp * 0x1p-63f;
+            float x[4], sx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float4 e = L[(xo & mask) + j];
+                x[j] = e.x;
+                sx[j] = e.y;
+            }
+            zg_rows<KIND, 8>(acc, racc, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
+                             amp * g[od.pitch + 1]);
+        }
+        // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
+        for (int q = 0; q < args.ngroup[kGBlk4]; ++q) {
+            const OctDev& od = args.oct[args.group[kGBlk4][q]];
+            const float4* L = args.lut + od.lut_off;  // 4 entries: x = 1/8, 3/8, 5/8, 7/8
+            const int pitch = od.pitch;
+            const float* g = grid + od.goff + (r0 >> 2) * pitch + (c0 >> 2);
+            const float amp = od.amp * 0x1p-63f;
+            float x[4], sx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float4 e = L[j];
+                x[j] = e.x;
+                sx[j] = e.y;
+            }
+            const float a0 = amp * g[0], a1 = amp * g[1];
+            const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
+            const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
+            zg_rows<KIND, 4>(acc, racc, 0, L, x, sx, a0, a1, b0, b1);
+            zg_rows<KIND, 4>(acc, racc, 4, L, x, sx, b0, b1, e0, e1);
+        }
+        // ppc == 2: columns (0,1) | (2,3) are two cells at x = 0.25, 0.75;
+        // rows pair up the same way; 3 corners per corner row.
+        for (int q = 0; q < args.ngroup[kGBlk2]; ++q) {
+            const OctDev& od = args.oct[args.group[kGBlk2][q]];
+            const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
+            const int pitch = od.pitch;
+            const float amp = od.amp * 0x1p-63f;
+            const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
+            float t0 = amp * g[0], t1 = amp * g[1], t2 = amp * g[2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float* gn = g + (k + 1) * pitch;
+                const float b0 = amp * gn[0], b1 = amp * gn[1], b2 = amp * gn[2];
+                Cell<KIND> ca, cb;
+                ca.make(&t0, &t1, &b0, &b1);
+                cb.make(&t1, &t2, &b1, &b2);
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const float4 f = rr ? e1 : e0;
+                    const auto ra = ca.row(f.x, f.y);
+                    const auto rb = cb.row(f.x, f.y);
+                    const int r = 2 * k + rr;
+                    acc[r][0] += Cell<KIND>::eval(ra, e0.x, e0.y, e0.w);
+                    acc[r][1] += Cell<KIND>::eval(ra, e1.x, e1.y, e1.w);
+                    acc[r][2] += Cell<KIND>::eval(rb, e0.x, e0.y, e0.w);
+                    acc[r][3] += Cell<KIND>::eval(rb, e1.x, e1.y, e1.w);
+                }
+                t0 = b0;
+                t1 = b1;
+                t2 = b2;
+            }
+        }
+        // ppc == 1: mean of 4 corners, amp/4 folded into the accumulate
+        for (int q = 0; q < args.ngroup[kGPpc1]; ++q) {
+            const OctDev& od = args.oct[args.group[kGPpc1][q]];
+            const float* g = grid + od.goff + r0 * od.pitch + c0;
+            const int pitch = od.pitch;
+            ppc1_block(acc, 0.25f * (od.amp * 0x1p-63f), [&](int r, float (&h)[5]) {
+                const float4 v = *reinterpret_cast<const float4*>(g + r * pitch);
+                h[0] = v.x;
+                h[1] = v.y;
+                h[2] = v.z;
+                h[3] = v.w;
+                h[4] = g[r * pitch + 4];
+            });
+        }
+    }
 
-        if (mode == kModeSubInt) {
-            // Lattice-point samples: zg and generic contribute h(ix, iy)
-            // exactly, Perlin exactly 0 (SURVEY §8c "exact shortcuts").
-            if (KIND == kPerlin || args.zero) continue;
+    // lattice-point octaves: zg and generic contribute h(ix, iy) exactly,
+    // Perlin exactly 0 (SURVEY §8c "exact shortcuts")
+    if constexpr (KIND != kPerlin) {
+        for (int q = 0; q < args.ngroup[kGSub]; ++q) {
+            const OctDev& od = args.oct[args.group[kGSub][q]];
             const float amp = od.amp * 0x1p-63f;  // exact power-of-two rescale
             const int64_t k = od.k, half = od.k >> 1;
             uint64_t X[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                X[j] = static_cast<uint64_t>((tx0 + c0 + j) * k + half) * kIxMul;
-            uint64_t Y = base + static_cast<uint64_t>((ty0 + r0) * k + half) * kIyMul;
+            for (int j = 0; j < 4; ++j) X[j] = static_cast<uint64_t>((tx0 + c0 + j) * k + half) * kIxMul;
+            uint64_t Y = seed_key + od.oct_key + static_cast<uint64_t>((ty0 + r0) * k + half) * kIyMul;
             const uint64_t dY = static_cast<uint64_t>(k) * kIyMul;
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
@@ -417,60 +517,19 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, height_scaled(add64(X[j], Y)), acc[r][j]);
                 Y = add64(Y, dY);
             }
-            continue;
         }
+    }
 
-        if constexpr (kZg) {
-            if (mode == kModePpc1) {
-                const float* g = grid + od.goff + r0 * od.pitch + c0;
-                const int pitch = od.pitch;
-                ppc1_block(acc, [&](int r, float (&h)[5]) {
-                    const float4 v = *reinterpret_cast<const float4*>(g + r * pitch);
-                    h[0] = v.x;
-                    h[1] = v.y;
-                    h[2] = v.z;
-                    h[3] = v.w;
-                    h[4] = g[r * pitch + 4];
-                });
-                continue;
-            }
-            if (mode == kModeBlock2) {
-                // 2 px per cell: columns (0,1) | (2,3) are two cells at x = 0.25,
-                // 0.75; rows pair up the same way.  3 corners per corner row.
-                const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
-                const int pitch = od.pitch;
-                const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
-                float t0 = g[0], t1 = g[1], t2 = g[2];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float* gn = g + (q + 1) * pitch;
-                    const float b0 = gn[0], b1 = gn[1], b2 = gn[2];
-                    Cell<KIND> ca, cb;
-                    ca.make(&t0, &t1, &b0, &b1);
-                    cb.make(&t1, &t2, &b1, &b2);
-#pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
-                        const float4 f = rr ? e1 : e0;
-                        const auto ra = ca.row(f.x, f.y);
-                        const auto rb = cb.row(f.x, f.y);
-                        const int r = 2 * q + rr;
-                        acc[r][0] += Cell<KIND>::eval(ra, e0.x, e0.y, e0.w);
-                        acc[r][1] += Cell<KIND>::eval(ra, e1.x, e1.y, e1.w);
-                        acc[r][2] += Cell<KIND>::eval(rb, e0.x, e0.y, e0.w);
-                        acc[r][3] += Cell<KIND>::eval(rb, e1.x, e1.y, e1.w);
-                    }
-                    t0 = b0;
-                    t1 = b1;
-                    t2 = b2;
-                }
-                continue;
-            }
-        }
+    // everything else: Perlin/generic cells, general (non-dividing/fractional) octaves
+    for (int q = 0; q < args.ngroup[kGGen]; ++q) {
+        const OctDev& od = args.oct[args.group[kGGen][q]];
+        const int mode = od.mode;
+        const uint64_t base = seed_key + od.oct_key;
+        // grids of zg octaves hold raw heights: scale at load
+        const float gscale = kZg ? od.amp * 0x1p-63f : 1.0f;
 
         if (mode == kModeBlock) {
-            // Power-of-two ppc >= 4 on the aligned tile grid: the thread's 4
-            // columns share one cell; its 8 rows change cell row only every ppc
-            // rows (never when ppc >= 8).  Sampling values from the row LUT.
+            // Perlin/generic, power-of-two ppc >= 4: 4 columns share one cell
             const int sh = od.shift, mask = od.ppc - 1;
             const float4* L = args.lut + od.lut_off;
             const int xo = static_cast<int>(tx0 & mask) + c0;
@@ -478,90 +537,36 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const int pitch = od.pitch;
             const float* g = grid + od.goff + (xo >> sh);
             float x[4], sx[4], xs[4];
-            const float4* Lx = L + (xo & mask);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float4 e = Lx[j];
+                const float4 e = L[(xo & mask) + j];
                 x[j] = e.x;
                 sx[j] = e.y;
                 xs[j] = e.w;
             }
-            if constexpr (kZg) {
-                // v = c0 + sx*c1 (+ x*c2): c0 is common to the 4 columns and goes
-                // into the per-row accumulator once per row.
-                const float4* Ly = L + (yo & mask);
-                const float* q = g + (yo >> sh) * pitch;
-                if (sh >= 3) {
-                    // ppc >= 8: the 4 x 8 block lies in one cell
-                    float h00, h10, h01, h11;
-                    h00 = q[0];
-                    h10 = q[1];
-                    h01 = q[pitch];
-                    h11 = q[pitch + 1];
-                    const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+            Cell<KIND> cell;
+            int last = -1;
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const float4 f = Ly[r];
-                        racc[r] += fmaf(f.y, dy, h00);
-                        if constexpr (KIND == kZgPaper) {
-                            const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
+            for (int r = 0; r < 8; ++r) {
+                const int yr = yo + r;
+                const int ry = yr >> sh;
+                const float4 f = L[yr & mask];
+                if (ry != last) {
+                    const int key = ry * pitch;
+                    float k00[CH], k10[CH], k01[CH], k11[CH];
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j]));
-                        } else {
-                            const float c1 = fmaf(a, f.y, dx);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(sx[j], c1, acc[r][j]);
-                        }
+                    for (int c = 0; c < CH; ++c) {
+                        k00[c] = gscale * g[c * kGridCap + key];
+                        k10[c] = gscale * g[c * kGridCap + key + 1];
+                        k01[c] = gscale * g[c * kGridCap + key + pitch];
+                        k11[c] = gscale * g[c * kGridCap + key + pitch + 1];
                     }
-                } else {
-                    // ppc == 4: rows 0-3 and 4-7 are two cell rows
-#pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        const float* qh = q + half * pitch;
-                        const float h00 = qh[0], h10 = qh[1], h01 = qh[pitch], h11 = qh[pitch + 1];
-                        const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
-#pragma unroll
-                        for (int rr = 0; rr < 4; ++rr) {
-                            const int r = 4 * half + rr;
-                            const float4 f = L[rr];
-                            racc[r] += fmaf(f.y, dy, h00);
-                            if constexpr (KIND == kZgPaper) {
-                                const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j]));
-                            } else {
-                                const float c1 = fmaf(a, f.y, dx);
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(sx[j], c1, acc[r][j]);
-                            }
-                        }
-                    }
+                    cell.make(k00, k10, k01, k11);
+                    last = ry;
                 }
-            } else {
-                Cell<KIND> cell;
-                int last = -1;
+                const auto row = cell.row(f.x, f.y);
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const int yr = yo + r;
-                    const int ry = yr >> sh;
-                    const float4 f = L[yr & mask];
-                    if (ry != last) {
-                        const int key = ry * pitch;
-                        float k00[CH], k10[CH], k01[CH], k11[CH];
-#pragma unroll
-                        for (int c = 0; c < CH; ++c) {
-                            k00[c] = g[c * kGridCap + key];
-                            k10[c] = g[c * kGridCap + key + 1];
-                            k01[c] = g[c * kGridCap + key + pitch];
-                            k11[c] = g[c * kGridCap + key + pitch + 1];
-                        }
-                        cell.make(k00, k10, k01, k11);
-                        last = ry;
-                    }
-                    const auto row = cell.row(f.x, f.y);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
-                }
+                for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
             }
             continue;
         }
@@ -593,10 +598,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                         float k00[CH], k10[CH], k01[CH], k11[CH];
 #pragma unroll
                         for (int c = 0; c < CH; ++c) {
-                            k00[c] = g[c * kGridCap + key];
-                            k10[c] = g[c * kGridCap + key + 1];
-                            k01[c] = g[c * kGridCap + key + pitch];
-                            k11[c] = g[c * kGridCap + key + pitch + 1];
+                            k00[c] = gscale * g[c * kGridCap + key];
+                            k10[c] = gscale * g[c * kGridCap + key + 1];
+                            k01[c] = gscale * g[c * kGridCap + key + pitch];
+                            k11[c] = gscale * g[c * kGridCap + key + pitch + 1];
                         }
                         cell.make(k00, k10, k01, k11);
                         last_key = key;
@@ -611,10 +616,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                         float k00[CH], k10[CH], k01[CH], k11[CH];
 #pragma unroll
                         for (int c = 0; c < CH; ++c) {
-                            k00[c] = g[c * kGridCap + key];
-                            k10[c] = g[c * kGridCap + key + 1];
-                            k01[c] = g[c * kGridCap + key + pitch];
-                            k11[c] = g[c * kGridCap + key + pitch + 1];
+                            k00[c] = gscale * g[c * kGridCap + key];
+                            k10[c] = gscale * g[c * kGridCap + key + 1];
+                            k01[c] = gscale * g[c * kGridCap + key + pitch];
+                            k11[c] = gscale * g[c * kGridCap + key + pitch + 1];
                         }
                         Cell<KIND> cj;
                         cj.make(k00, k10, k01, k11);
@@ -629,10 +634,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
         const float amp = od.amp;
         if constexpr (kZg) {
             if (od.cls == kClsFast && od.ppc == 1) {
-                ppc1_block(acc, [&](int r, float (&h)[5]) {
+                ppc1_block(acc, 0.25f, [&](int r, float (&h)[5]) {
 #pragma unroll
-                    for (int q = 0; q < 5; ++q)
-                        corner_data<KIND>(base, tx0 + c0 + q, ty0 + r0 + r, amp, od.w, args.zero, &h[q]);
+                    for (int k = 0; k < 5; ++k)
+                        corner_data<KIND>(base, tx0 + c0 + k, ty0 + r0 + r, amp, od.w, &h[k]);
                 });
                 continue;
             }
@@ -655,10 +660,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     float k00[CH], k10[CH], k01[CH], k11[CH];
-                    corner_data<KIND>(base, cxi[j], iy, amp, od.w, args.zero, k00);
-                    corner_data<KIND>(base, cxi[j] + 1, iy, amp, od.w, args.zero, k10);
-                    corner_data<KIND>(base, cxi[j], iy + 1, amp, od.w, args.zero, k01);
-                    corner_data<KIND>(base, cxi[j] + 1, iy + 1, amp, od.w, args.zero, k11);
+                    corner_data<KIND>(base, cxi[j], iy, amp, od.w, k00);
+                    corner_data<KIND>(base, cxi[j] + 1, iy, amp, od.w, k10);
+                    corner_data<KIND>(base, cxi[j], iy + 1, amp, od.w, k01);
+                    corner_data<KIND>(base, cxi[j] + 1, iy + 1, amp, od.w, k11);
                     Cell<KIND> cj;
                     cj.make(k00, k10, k01, k11);
                     const float v = Cell<KIND>::eval(cj.row(y, sy), x[j], sx[j], xs[j]);
@@ -673,7 +678,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     // ---- single fp32 store of the finished tile ----------------------------
     const int64_t lx0 = tx0 + c0 - args.ox;
     const int64_t ly0 = ty0 + r0 - args.oy;
-    float* row = out + static_cast<int64_t>(map) * args.map_stride + ly0 * args.ld + lx0;
+    float* row = out + static_cast<int64_t>(blockIdx.z) * args.map_stride + ly0 * args.ld + lx0;
     const bool vec_ok = ((lx0 & 3) == 0) && ((args.ld & 3) == 0) && ((args.map_stride & 3) == 0) &&
                         ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && lx0 >= 0 &&
                         lx0 + 4 <= args.width;

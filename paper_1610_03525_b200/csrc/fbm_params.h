@@ -64,6 +64,22 @@ struct OctDev {
     int32_t pad;
 };
 
+// Octave lists built by the host planner (capi.cu): the kernel loops over
+// mode-homogeneous lists instead of dispatching per octave.  Accumulation
+// order is therefore group order — fixed per configuration, so results stay
+// a pure function of (config, pixel).
+enum OctGroup : int32_t {
+    kGProCoarse = 0,  // aligned grids of <= 32 corners: one warp per octave
+    kGProFine = 1,    // other grids / sampling tables
+    kGBlk8 = 2,       // zg, power-of-two ppc >= 8
+    kGBlk4 = 3,       // zg, ppc == 4
+    kGBlk2 = 4,       // zg, ppc == 2
+    kGPpc1 = 5,       // zg, ppc == 1
+    kGSub = 6,        // lattice-point octaves
+    kGGen = 7,        // everything else (Perlin/generic cells, general octaves)
+    kNumGroups = 8
+};
+
 struct FbmArgs {
     int64_t ox, oy;          // window origin, global pixels
     int64_t tile_x0, tile_y0;  // tile-grid origin (aligned to the tile size in global px)
@@ -79,6 +95,8 @@ struct FbmArgs {
     // lut[2^k - 1 + r] = (x, S(x), S(x) - x, x*S(x)) with x = (r + 0.5)/ppc
     // (kernels2d.hpp:214-239 at phase 0.5), computed in fp64 and rounded.
     const float4* lut;
+    int32_t ngroup[kNumGroups];
+    int8_t group[kNumGroups][kMaxOctaves];
     uint64_t seed_key[kMaxBatch];  // seed * K1 per map (lattice.hpp:47)
     OctDev oct[kMaxOctaves];
 };
