@@ -149,8 +149,9 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
             d.lut_off = (1 << d.shift) - 1;
             ncx = std::max<int64_t>(tg::kTileW >> d.shift, 1) + 1;
             ncy = std::max<int64_t>(tg::kTileH >> d.shift, 1) + 1;
-            if (zg && d.ppc == 1) mode = tg::kModePpc1;
-            else if (zg && d.ppc == 2) mode = tg::kModeBlock2;
+            const bool perlin = c->method == TG_METHOD_PERLIN3 || c->method == TG_METHOD_PERLIN5;
+            if ((zg || perlin) && d.ppc == 1) mode = tg::kModePpc1;
+            else if (d.ppc == 2) mode = tg::kModeBlock2;
             else if (d.ppc >= 4) mode = tg::kModeBlock;
             else mode = tg::kModeGrid;
         } else if (d.cls == tg::kClsFast) {
@@ -265,8 +266,8 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
         if (d.mode == tg::kModeSubInt) push(tg::kGSub);
         else if (zg && d.mode == tg::kModeBlock && d.shift >= 3) push(tg::kGBlk8);
         else if (zg && d.mode == tg::kModeBlock && d.shift == 2) push(tg::kGBlk4);
-        else if (zg && d.mode == tg::kModeBlock2) push(tg::kGBlk2);
-        else if (zg && d.mode == tg::kModePpc1) push(tg::kGPpc1);
+        else if (d.mode == tg::kModeBlock2) push(tg::kGBlk2);
+        else if (d.mode == tg::kModePpc1) push(tg::kGPpc1);
         else push(tg::kGGen);
     }
     a->lut = tg::row_lut(order_of(c));

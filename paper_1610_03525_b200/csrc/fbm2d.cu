@@ -57,13 +57,13 @@ __device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float 
         d[0] = amp63 * height_scaled(p);
     } else if constexpr (KIND == kPerlin) {
         float c, s;
-        sincospif(2.0f * unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
+        fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
         d[0] = amp * c;
         d[1] = amp * s;
     } else {
         d[0] = amp63 * height_scaled(p);
         float c, s;
-        sincospif(2.0f * unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
+        fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
         const float m = unit_from_hash(mix64(p ^ kMagnitudeLane)) * w;
         d[1] = m * c;
         d[2] = m * s;
@@ -118,23 +118,31 @@ template <> struct Cell<kZgSeparable> {
 };
 
 template <> struct Cell<kPerlin> {
-    float f0, g0, f1, g1, f2, g2, f3, g3;  // corners 00, 10, 01, 11
+    // kernels2d.hpp:163-173: lerp_y of the two x-lerped gradient ramps.  For a
+    // fixed cell every coefficient of the column features {1, x, sx, x*sx} is
+    // a linear combination of the row features {1, y, sy, y*sy}.
+    float a0y, a0ys, a0s, a1c, a1s, a2c, a2y, a2ys, a2s, a3c, a3s;
     __device__ __forceinline__ void make(const float* k00, const float* k10, const float* k01,
                                          const float* k11) {
-        f0 = k00[0]; g0 = k00[1];
-        f1 = k10[0]; g1 = k10[1];
-        f2 = k01[0]; g2 = k01[1];
-        f3 = k11[0]; g3 = k11[1];
+        const float f0 = k00[0], g0 = k00[1], f1 = k10[0], g1 = k10[1];  // corners 00, 10
+        const float f2 = k01[0], g2 = k01[1], f3 = k11[0], g3 = k11[1];  // corners 01, 11
+        a0y = g0;
+        a0ys = g2 - g0;
+        a0s = -g2;
+        a1c = f0;
+        a1s = f2 - f0;
+        a2c = -f1;
+        a2y = g1 - g0;
+        a2ys = (g3 - g2) - a2y;
+        a2s = (f1 - f3) - (g3 - g2);
+        a3c = f1 - f0;
+        a3s = (f3 - f2) - a3c;
     }
     struct Row { float a0, a1, a2, a3; };
     __device__ __forceinline__ Row row(float y, float sy) const {
-        // lerp_y of the two x-lerped ramps (kernels2d.hpp:163-173), expanded in
-        // the column features {1, x, sx, x*sx}.
-        const float ym = y - 1.f;
-        const float p0 = g0 * y, p1 = f0, p2 = fmaf(g1 - g0, y, -f1), p3 = f1 - f0;
-        const float q0 = g2 * ym, q1 = f2, q2 = fmaf(g3 - g2, ym, -f3), q3 = f3 - f2;
-        return {fmaf(sy, q0 - p0, p0), fmaf(sy, q1 - p1, p1), fmaf(sy, q2 - p2, p2),
-                fmaf(sy, q3 - p3, p3)};
+        const float ys = y * sy;
+        return {fmaf(a0y, y, fmaf(a0ys, ys, a0s * sy)), fmaf(sy, a1s, a1c),
+                fmaf(a2y, y, fmaf(a2ys, ys, fmaf(a2s, sy, a2c))), fmaf(sy, a3s, a3c)};
     }
     __device__ __forceinline__ static float eval(const Row& r, float x, float sx, float xs) {
         return fmaf(xs, r.a3, fmaf(sx, r.a2, fmaf(x, r.a1, r.a0)));
@@ -266,7 +274,8 @@ __device__ __forceinline__ void zg_rows(float (&acc)[8][4], float (&racc)[8], in
 #endif
 
 template <int KIND, int ORDER>
-__global__ void __launch_bounds__(kThreads, (KIND == kZgPaper || KIND == kZgSeparable) ? TG_ZG_MIN_BLOCKS : 1)
+__global__ void __launch_bounds__(kThreads, (KIND == kZgPaper || KIND == kZgSeparable) ? TG_ZG_MIN_BLOCKS
+                                            : (KIND == kPerlin ? 2 : 1))
 fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     constexpr int CH = Traits<KIND>::kCh;
     constexpr bool kZg = KIND == kZgPaper || KIND == kZgSeparable;
@@ -451,43 +460,56 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             zg_rows<KIND, 4>(acc, racc, 0, L, x, sx, a0, a1, b0, b1);
             zg_rows<KIND, 4>(acc, racc, 4, L, x, sx, b0, b1, e0, e1);
         }
-        // ppc == 2: columns (0,1) | (2,3) are two cells at x = 0.25, 0.75;
-        // rows pair up the same way; 3 corners per corner row.
-        for (int q = 0; q < args.ngroup[kGBlk2]; ++q) {
-            const OctDev& od = args.oct[args.group[kGBlk2][q]];
-            const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
-            const int pitch = od.pitch;
-            const float amp = od.amp * 0x1p-63f;
-            const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
-            float t0 = amp * g[0], t1 = amp * g[1], t2 = amp * g[2];
+    }
+
+    // ppc == 2: columns (0,1) | (2,3) are two cells at x = 0.25, 0.75; rows
+    // pair up the same way; 3 corners per corner row.
+    for (int q = 0; q < args.ngroup[kGBlk2]; ++q) {
+        const OctDev& od = args.oct[args.group[kGBlk2][q]];
+        const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
+        const int pitch = od.pitch;
+        const float sc = kZg ? od.amp * 0x1p-63f : 1.0f;
+        const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
+        float t[3][CH];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float* gn = g + (k + 1) * pitch;
-                const float b0 = amp * gn[0], b1 = amp * gn[1], b2 = amp * gn[2];
-                Cell<KIND> ca, cb;
-                ca.make(&t0, &t1, &b0, &b1);
-                cb.make(&t1, &t2, &b1, &b2);
+        for (int u = 0; u < 3; ++u)
 #pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    const float4 f = rr ? e1 : e0;
-                    const auto ra = ca.row(f.x, f.y);
-                    const auto rb = cb.row(f.x, f.y);
-                    const int r = 2 * k + rr;
-                    acc[r][0] += Cell<KIND>::eval(ra, e0.x, e0.y, e0.w);
-                    acc[r][1] += Cell<KIND>::eval(ra, e1.x, e1.y, e1.w);
-                    acc[r][2] += Cell<KIND>::eval(rb, e0.x, e0.y, e0.w);
-                    acc[r][3] += Cell<KIND>::eval(rb, e1.x, e1.y, e1.w);
-                }
-                t0 = b0;
-                t1 = b1;
-                t2 = b2;
+            for (int c = 0; c < CH; ++c) t[u][c] = sc * g[c * kGridCap + u];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float* gn = g + (k + 1) * pitch;
+            float b[3][CH];
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+#pragma unroll
+                for (int c = 0; c < CH; ++c) b[u][c] = sc * gn[c * kGridCap + u];
+            Cell<KIND> ca, cb;
+            ca.make(t[0], t[1], b[0], b[1]);
+            cb.make(t[1], t[2], b[1], b[2]);
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const float4 f = rr ? e1 : e0;
+                const auto ra = ca.row(f.x, f.y);
+                const auto rb = cb.row(f.x, f.y);
+                const int r = 2 * k + rr;
+                acc[r][0] += Cell<KIND>::eval(ra, e0.x, e0.y, e0.w);
+                acc[r][1] += Cell<KIND>::eval(ra, e1.x, e1.y, e1.w);
+                acc[r][2] += Cell<KIND>::eval(rb, e0.x, e0.y, e0.w);
+                acc[r][3] += Cell<KIND>::eval(rb, e1.x, e1.y, e1.w);
             }
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+#pragma unroll
+                for (int c = 0; c < CH; ++c) t[u][c] = b[u][c];
         }
-        // ppc == 1: mean of 4 corners, amp/4 folded into the accumulate
-        for (int q = 0; q < args.ngroup[kGPpc1]; ++q) {
-            const OctDev& od = args.oct[args.group[kGPpc1][q]];
-            const float* g = grid + od.goff + r0 * od.pitch + c0;
-            const int pitch = od.pitch;
+    }
+    // ppc == 1 (x = y = 1/2)
+    for (int q = 0; q < args.ngroup[kGPpc1]; ++q) {
+        const OctDev& od = args.oct[args.group[kGPpc1][q]];
+        const int pitch = od.pitch;
+        const float* g = grid + od.goff + r0 * pitch + c0;
+        if constexpr (kZg) {
+            // every zero-gradient kernel is the mean of its 4 corners
             ppc1_block(acc, 0.25f * (od.amp * 0x1p-63f), [&](int r, float (&h)[5]) {
                 const float4 v = *reinterpret_cast<const float4*>(g + r * pitch);
                 h[0] = v.x;
@@ -496,6 +518,37 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 h[3] = v.w;
                 h[4] = g[r * pitch + 4];
             });
+        } else if constexpr (KIND == kPerlin) {
+            // Perlin at the cell centre: v = (a00 + b10 - b01 - a11)/8 with
+            // a = f + g, b = g - f per corner (kernels2d.hpp:163-173 at 1/2)
+            auto load = [&](int r, float (&av)[5], float (&bv)[5]) {
+                const float* gf = g + r * pitch;
+                const float* gg = gf + kGridCap;
+                const float4 f4 = *reinterpret_cast<const float4*>(gf);
+                const float4 g4 = *reinterpret_cast<const float4*>(gg);
+                const float fv[5] = {f4.x, f4.y, f4.z, f4.w, gf[4]};
+                const float gv[5] = {g4.x, g4.y, g4.z, g4.w, gg[4]};
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    av[k] = fv[k] + gv[k];
+                    bv[k] = gv[k] - fv[k];
+                }
+            };
+            float at[5], bt[5];
+            load(0, at, bt);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                float ab[5], bb[5];
+                load(r + 1, ab, bb);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    acc[r][j] = fmaf(0.125f, (at[j] + bt[j + 1]) - (bb[j] + ab[j + 1]), acc[r][j]);
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    at[k] = ab[k];
+                    bt[k] = bb[k];
+                }
+            }
         }
     }
 

@@ -105,6 +105,14 @@ __device__ __forceinline__ float unit_from_hash(uint64_t z) {
     return static_cast<float>(static_cast<uint32_t>(z >> 32)) * 0x1p-32f;
 }
 
+// (sin, cos)(2*pi*u) for u in [0, 1] turns with the hardware approximations
+// on the centred angle 2*pi*(u - [u >= 1/2]) in [-pi, pi), where their
+// absolute error is ~2^-21.4 (components checked within tolerance).
+__device__ __forceinline__ void fast_sincos_turns(float u, float* s, float* c) {
+    const float v = u >= 0.5f ? u - 1.0f : u;
+    __sincosf(6.28318530717958647692f * v, s, c);
+}
+
 __device__ __forceinline__ float corner_height(uint64_t base, int64_t ix, int64_t iy) {
     return height_scaled(pack_xy(base, ix, iy)) * 0x1p-63f;
 }
@@ -114,7 +122,7 @@ __device__ __forceinline__ float corner_height(uint64_t base, int64_t ix, int64_
 __device__ __forceinline__ void corner_unit_gradient(uint64_t base, int64_t ix, int64_t iy,
                                                      float* c, float* s) {
     const uint64_t z = mix64(pack_xy(base, ix, iy) ^ kAngleLane);
-    sincospif(2.0f * unit_from_hash(z), s, c);
+    fast_sincos_turns(unit_from_hash(z), s, c);
 }
 
 // corner_gradient (lattice.hpp:72-77): magnitude uniform in [0, w].
@@ -122,7 +130,7 @@ __device__ __forceinline__ void corner_gradient(uint64_t base, int64_t ix, int64
                                                 float* gx, float* gy) {
     const uint64_t p = pack_xy(base, ix, iy);
     float c, s;
-    sincospif(2.0f * unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
+    fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
     const float m = unit_from_hash(mix64(p ^ kMagnitudeLane)) * w;
     *gx = m * c;
     *gy = m * s;
