@@ -23,6 +23,7 @@ cudaError_t fbm2d_launch(int kind, int order, const FbmArgs& a, float* out, cuda
 int fbm2d_tile_h();
 cudaError_t fbm3d_launch(int order, const Fbm3Args& a, float* out, cudaStream_t st);
 void fbm3d_tile(int* tx, int* ty, int* tz);
+void fbm3d_plan(Fbm3Args* a, int zg_sep_only);
 cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uint64_t lane,
                            void* out, cudaStream_t st);
 cudaError_t widen_launch(const float* in, double* out, uint64_t n, cudaStream_t st);
@@ -463,6 +464,9 @@ int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int6
     const int64_t cand[6] = {ox - 64, ox + nx + 64, oy - 64, oy + ny + 64, oz - 64, oz + nz + 64};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
     plan_octaves(cfg, gmax, a.oct, false);
+    tg::fbm3d_plan(&a, 1);
+    a.lut = tg::row_lut(order_of(cfg));
+    if (!a.lut) return fail(TG_EDEVICE, "row LUT allocation failed");
     TG_CUDA(tg::fbm3d_launch(order_of(cfg), a, dev_out, static_cast<cudaStream_t>(stream)));
     return TG_OK;
 }

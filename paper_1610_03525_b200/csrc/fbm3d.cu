@@ -1,15 +1,24 @@
 // fbm3d.cu — fused-octave 3D fBm volume (new, the
-// reference has no 3D kernel).
+// reference has no 3D kernel: parity is property-pinned + restated oracle).
 //
 // Cell: separable zero-gradient trilinear blend with smoothstep weights,
 //   v = lerp_z(lerp_y(lerp_x(h, Sx), Sy), Sz),
 // which reduces on every face to kernels2d::zg_eval(..., separable) and has
-// zero gradient at all 8 corners.  Lattice key: pack2 + iz * K5 (iz = 0 is
-// the 2D lattice).  Per axis the sampling is the 2D rule (fast: x = (r+0.5)/ppc,
-// else ((g+0.5)/R)*freq in fp64).  Same tile/shared-corner structure as
-// fbm2d.cu: a 128 x 8 x 8 voxel tile, accumulators in registers over all
-// octaves, one fp32 store per voxel.
+// zero gradient at all 8 corners.  Lattice key: pack2 + iz * K5 (iz = 0 is the
+// 2D lattice).  Per axis the sampling is the 2D rule (fast: x = (r+0.5)/ppc,
+// else ((g+0.5)/R)*freq in fp64).
+//
+// Same structure as fbm2d.cu: a 128 x 8 x 8 voxel tile per CTA (thread = 4
+// columns x 1 row x 8 slices), one prologue hashing every octave's unique
+// corners into shared memory, one barrier, then per-octave evaluation with
+// the cell factorised per (cell, y, z):  v(x) = B0 + Sx*(B1 - B0), the
+// y-lerps hoisted per cell and B0 accumulated once per (y, z) when the
+// thread's 4 columns share a cell.  Lattice-point octaves hash one corner per
+// voxel; ppc = 1 is the mean of 8 corners.  Accumulators stay in registers;
+// one fp32 store per voxel.
 #include <cuda_runtime.h>
+
+#include <cmath>
 
 #include "fbm_params.h"
 #include "lattice.cuh"
@@ -20,7 +29,7 @@ namespace {
 
 constexpr int kThreads3 = 256;
 constexpr int kTX = 128, kTY = 8, kTZ = 8;
-constexpr int kCap3 = (kTX + 2) * (kTY + 2) * (kTZ + 2);
+constexpr int kCap3 = 13312;  // corner floats per CTA
 
 template <int ORDER>
 __device__ __forceinline__ float smooth3(float t) {
@@ -52,26 +61,35 @@ __device__ __forceinline__ void coord3(const OctDev& od, double R, int64_t g, in
     }
 }
 
-__device__ __forceinline__ float h3(uint64_t base, int64_t ix, int64_t iy, int64_t iz, float amp,
-                                    int zero) {
-    if (zero) return 0.f;
-    const uint64_t p = base + static_cast<uint64_t>(ix) * kIxMul + static_cast<uint64_t>(iy) * kIyMul +
-                       static_cast<uint64_t>(iz) * kIzMul;
-    return amp * height_from_hash(mix64(p));
+__device__ __forceinline__ uint64_t pack3(uint64_t base, int64_t ix, int64_t iy, int64_t iz) {
+    return base + static_cast<uint64_t>(ix) * kIxMul + static_cast<uint64_t>(iy) * kIyMul +
+           static_cast<uint64_t>(iz) * kIzMul;
 }
-
-struct Smem3 {
-    float xs[kTX], xv[kTX];
-    int64_t xi[kTX];
-    float ys[kTY], zs[kTZ];
-    int64_t yi[kTY], zi[kTZ];
-    float grid[kCap3];
-};
 
 __device__ __forceinline__ float lerp(float a, float b, float s) { return fmaf(s, b - a, a); }
 
+// One plan entry per octave is computed by the host (capi.cu plan3):
+// mode in OctDev.mode, grid shape ncx, ncy, pad(=ncz), pitch (x stride), goff.
+enum Mode3 : int32_t { kM3Sub = 0, kM3P1 = 1, kM3Blk = 2, kM3Gen = 3, kM3Direct = 4 };
+
+struct Tab3 {
+    float xt[kTX], xs[kTX];
+    int32_t xi[kTX];
+    float yt[kTY], ys[kTY];
+    int32_t yi[kTY];
+    float zt[kTZ], zs[kTZ];
+    int32_t zi[kTZ];
+};
+
+constexpr int kTabs3 = 2;
+
+struct Smem3 {
+    Tab3 tab[kTabs3];
+    float grid[kCap3];
+};
+
 template <int ORDER>
-__global__ void __launch_bounds__(kThreads3)
+__global__ void __launch_bounds__(kThreads3, 2)
 fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char raw3[];
     Smem3& S = *reinterpret_cast<Smem3*>(raw3);
@@ -80,110 +98,289 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     const int64_t ty0 = a.tile_y0 + static_cast<int64_t>(blockIdx.y) * kTY;
     const int64_t tz0 = a.tile_z0 + static_cast<int64_t>(blockIdx.z) * kTZ;
     const int c0 = lane * 4;
-    float acc[kTZ][4];
+
+    // ---- prologue: all octaves' tile corners (raw height_scaled values) ------
+    for (int o = 0; o < a.octaves; ++o) {
+        const OctDev& od = a.oct[o];
+        const int mode = od.mode;
+        if (mode == kM3Sub || mode == kM3Direct) continue;
+        const uint64_t base = a.seed_key + od.oct_key;
+        int64_t ix0, iy0, iz0;
+        int ncx = od.ncx, ncy = od.ncy, ncz = od.pad;
+        if (od.lut_off >= 0) {
+            ix0 = tx0 >> od.shift;
+            iy0 = ty0 >> od.shift;
+            iz0 = tz0 >> od.shift;
+        } else {
+            int64_t e;
+            float t;
+            coord3(od, a.R, tx0, &ix0, &t);
+            coord3(od, a.R, tx0 + kTX - 1, &e, &t);
+            ncx = static_cast<int>(e - ix0 + 2);
+            coord3(od, a.R, ty0, &iy0, &t);
+            coord3(od, a.R, ty0 + kTY - 1, &e, &t);
+            ncy = static_cast<int>(e - iy0 + 2);
+            coord3(od, a.R, tz0, &iz0, &t);
+            coord3(od, a.R, tz0 + kTZ - 1, &e, &t);
+            ncz = static_cast<int>(e - iz0 + 2);
+            Tab3& tb = S.tab[od.tslot];
+            if (tid < kTX) {
+                int64_t i;
+                float x;
+                coord3(od, a.R, tx0 + tid, &i, &x);
+                tb.xi[tid] = static_cast<int32_t>(i - ix0);
+                tb.xt[tid] = x;
+                tb.xs[tid] = smooth3<ORDER>(x);
+            } else if (tid < kTX + kTY) {
+                const int r = tid - kTX;
+                int64_t i;
+                float y;
+                coord3(od, a.R, ty0 + r, &i, &y);
+                tb.yi[r] = static_cast<int32_t>(i - iy0);
+                tb.yt[r] = y;
+                tb.ys[r] = smooth3<ORDER>(y);
+            } else if (tid < kTX + kTY + kTZ) {
+                const int r = tid - kTX - kTY;
+                int64_t i;
+                float z;
+                coord3(od, a.R, tz0 + r, &i, &z);
+                tb.zi[r] = static_cast<int32_t>(i - iz0);
+                tb.zt[r] = z;
+                tb.zs[r] = smooth3<ORDER>(z);
+            }
+        }
+        const uint64_t p0 = pack3(base, ix0, iy0, iz0);
+        const int pitch = od.pitch, plane = pitch * od.ncy;  // strides use the planned bounds
+        float* g = S.grid + od.goff;
+        const int nrows = ncy * ncz;
+        if (od.lut_off >= 0 && od.shift == 0) {
+            // ppc = 1: 129 x 9 x 9 corners; 4 consecutive x per lane (four hash
+            // chains, one 16-byte store), the last column through a flat loop.
+            const uint64_t px = p0 + static_cast<uint64_t>(4 * lane) * kIxMul;
+            for (int rw = warp; rw < nrows; rw += kThreads3 / 32) {
+                const int cz = rw / ncy, cy = rw - cz * ncy;
+                const uint64_t p = px + static_cast<uint64_t>(cy) * kIyMul + static_cast<uint64_t>(cz) * kIzMul;
+                float4 v;
+                v.x = height_scaled(p);
+                v.y = height_scaled(add64(p, kIxMul));
+                v.z = height_scaled(add64(p, 2 * kIxMul));
+                v.w = height_scaled(add64(p, 3 * kIxMul));
+                *reinterpret_cast<float4*>(g + cz * plane + cy * pitch + 4 * lane) = v;
+            }
+            for (int rw = tid; rw < nrows; rw += kThreads3) {
+                const int cz = rw / ncy, cy = rw - cz * ncy;
+                g[cz * plane + cy * pitch + kTX] =
+                    height_scaled(p0 + static_cast<uint64_t>(kTX) * kIxMul + static_cast<uint64_t>(cy) * kIyMul +
+                                  static_cast<uint64_t>(cz) * kIzMul);
+            }
+        } else {
+            const int n = ncx * nrows;
+            const float rx = 1.0f / static_cast<float>(ncx), ry = 1.0f / static_cast<float>(ncy);
+            for (int i0 = tid; i0 < n; i0 += 4 * kThreads3) {
+                float d[4];
+                int dst[4];
 #pragma unroll
-    for (int z = 0; z < kTZ; ++z)
+                for (int u = 0; u < 4; ++u) {
+                    const int i = min(i0 + u * kThreads3, n - 1);
+                    const int rw = static_cast<int>((static_cast<float>(i) + 0.5f) * rx);
+                    const int cx = i - rw * ncx;
+                    const int cz = static_cast<int>((static_cast<float>(rw) + 0.5f) * ry);
+                    const int cy = rw - cz * ncy;
+                    dst[u] = cz * plane + cy * pitch + cx;
+                    d[u] = height_scaled(pack3(p0, cx, cy, cz));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (i0 + u * kThreads3 < n) g[dst[u]] = d[u];
+            }
+        }
+    }
+    __syncthreads();
+
+    float acc[kTZ][4], racc[kTZ];
+#pragma unroll
+    for (int z = 0; z < kTZ; ++z) {
+        racc[z] = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[z][j] = 0.f;
+    }
 
     for (int o = 0; o < a.octaves; ++o) {
         const OctDev& od = a.oct[o];
+        const int mode = od.mode;
+        const float amp = od.amp * 0x1p-63f;
         const uint64_t base = a.seed_key + od.oct_key;
-        if (od.cls == kClsSubInt) {  // samples on lattice points: v = h(ix, iy, iz)
-            if (a.zero) continue;
+        const int pitch = od.pitch, plane = od.pitch * od.ncy;
+
+        if (mode == kM3Sub) {  // lattice points: v = h(ix, iy, iz)
             const int64_t k = od.k, half = od.k >> 1;
-            const int64_t iy = (ty0 + warp) * k + half;
+            const uint64_t Y = base + static_cast<uint64_t>((ty0 + warp) * k + half) * kIyMul;
+            uint64_t X[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) X[j] = add64(Y, static_cast<uint64_t>((tx0 + c0 + j) * k + half) * kIxMul);
+            uint64_t Z = static_cast<uint64_t>(tz0 * k + half) * kIzMul;
+            const uint64_t dZ = static_cast<uint64_t>(k) * kIzMul;
 #pragma unroll
             for (int z = 0; z < kTZ; ++z) {
-                const int64_t iz = (tz0 + z) * k + half;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(amp, height_scaled(add64(X[j], Z)), acc[z][j]);
+                Z = add64(Z, dZ);
+            }
+            continue;
+        }
+
+        if (mode == kM3P1) {  // x = y = z = 1/2: the mean of the 8 corners
+            const float* g = S.grid + od.goff + warp * pitch + c0;
+            const float q = 0.125f * amp;
+            auto face = [&](int z, float (&F)[4]) {
+                const float* r0p = g + z * plane;
+                const float* r1p = r0p + pitch;
+                const float4 u = *reinterpret_cast<const float4*>(r0p);
+                const float4 w = *reinterpret_cast<const float4*>(r1p);
+                const float u4 = r0p[4], w4 = r1p[4];
+                const float s0 = u.x + w.x, s1 = u.y + w.y, s2 = u.z + w.z, s3 = u.w + w.w, s4 = u4 + w4;
+                F[0] = s0 + s1;
+                F[1] = s1 + s2;
+                F[2] = s2 + s3;
+                F[3] = s3 + s4;
+            };
+            float Fa[4];
+            face(0, Fa);
+#pragma unroll
+            for (int z = 0; z < kTZ; ++z) {
+                float Fb[4];
+                face(z + 1, Fb);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int64_t ix = (tx0 + c0 + j) * k + half;
-                    acc[z][j] += h3(base, ix, iy, iz, od.amp, 0);
+                    acc[z][j] = fmaf(q, Fa[j] + Fb[j], acc[z][j]);
+                    Fa[j] = Fb[j];
                 }
             }
             continue;
         }
-        __syncthreads();
-        if (tid < kTX) {
-            int64_t i;
-            float t;
-            coord3(od, a.R, tx0 + tid, &i, &t);
-            S.xi[tid] = i;
-            S.xv[tid] = t;
-            S.xs[tid] = smooth3<ORDER>(t);
-        } else if (tid < kTX + kTY) {
-            const int r = tid - kTX;
-            int64_t i;
-            float t;
-            coord3(od, a.R, ty0 + r, &i, &t);
-            S.yi[r] = i;
-            S.ys[r] = smooth3<ORDER>(t);
-        } else if (tid < kTX + kTY + kTZ) {
-            const int r = tid - kTX - kTY;
-            int64_t i;
-            float t;
-            coord3(od, a.R, tz0 + r, &i, &t);
-            S.zi[r] = i;
-            S.zs[r] = smooth3<ORDER>(t);
-        }
-        int64_t ix0, ixe, iy0, iye, iz0, ize;
-        float d;
-        coord3(od, a.R, tx0, &ix0, &d);
-        coord3(od, a.R, tx0 + kTX - 1, &ixe, &d);
-        coord3(od, a.R, ty0, &iy0, &d);
-        coord3(od, a.R, ty0 + kTY - 1, &iye, &d);
-        coord3(od, a.R, tz0, &iz0, &d);
-        coord3(od, a.R, tz0 + kTZ - 1, &ize, &d);
-        const int64_t nx = ixe - ix0 + 2, ny = iye - iy0 + 2, nz = ize - iz0 + 2;
-        const bool direct = nx * ny * nz > kCap3;
-        const int ncx = static_cast<int>(nx), ncy = static_cast<int>(ny), ncz = static_cast<int>(nz);
-        if (!direct) {
-            const int planes = ncy * ncz;
-            for (int pl = warp; pl < planes; pl += kThreads3 / 32) {
-                const int cz = pl / ncy, cy = pl - cz * ncy;
-                for (int cx = lane; cx < ncx; cx += 32)
-                    S.grid[(cz * ncy + cy) * ncx + cx] = h3(base, ix0 + cx, iy0 + cy, iz0 + cz, od.amp, a.zero);
+
+        if (mode == kM3Blk) {  // power-of-two ppc >= 2 on the aligned tile grid
+            const int sh = od.shift, mask = od.ppc - 1;
+            const float4* L = a.lut + od.lut_off;
+            const int xo = static_cast<int>(tx0 & mask) + c0;
+            const int yo = static_cast<int>(ty0 & mask) + warp;
+            const int zo = static_cast<int>(tz0 & mask);
+            const float sy = L[yo & mask].y;
+            float sx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sx[j] = L[(xo + j) & mask].y;
+            const float* gy = S.grid + od.goff + (yo >> sh) * pitch;
+            if (sh >= 2) {
+                // the thread's 4 columns share one x-cell; B0 -> per-slice accumulator
+                const float* g = gy + (xo >> sh);
+                int last = -1;
+                float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+#pragma unroll
+                for (int z = 0; z < kTZ; ++z) {
+                    const int zr = zo + z, cz = zr >> sh;
+                    if (cz != last) {
+                        const float* q = g + cz * plane;
+                        // y-lerps of the x=0 / x=1 edges at z = cz, cz+1
+                        e0 = amp * lerp(q[0], q[pitch], sy);
+                        e1 = amp * lerp(q[plane], q[plane + pitch], sy);
+                        e2 = amp * lerp(q[1], q[pitch + 1], sy);
+                        e3 = amp * lerp(q[plane + 1], q[plane + pitch + 1], sy);
+                        last = cz;
+                    }
+                    const float sz = L[zr & mask].y;
+                    const float b0 = lerp(e0, e1, sz), d = lerp(e2, e3, sz) - b0;
+                    racc[z] += b0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(sx[j], d, acc[z][j]);
+                }
+            } else {
+                // ppc = 2: columns (0,1) and (2,3) are two x-cells
+                const float* g = gy + (xo >> 1);
+#pragma unroll
+                for (int zc = 0; zc < kTZ / 2; ++zc) {
+                    const float* q = g + ((zo >> 1) + zc) * plane;
+                    float e[3][2];  // y-lerped corner columns x = 0..2 at z = cz, cz+1
+#pragma unroll
+                    for (int u = 0; u < 3; ++u) {
+                        e[u][0] = amp * lerp(q[u], q[pitch + u], sy);
+                        e[u][1] = amp * lerp(q[plane + u], q[plane + pitch + u], sy);
+                    }
+#pragma unroll
+                    for (int zz = 0; zz < 2; ++zz) {
+                        const int z = 2 * zc + zz;
+                        const float sz = L[(zo + z) & mask].y;
+                        const float b0 = lerp(e[0][0], e[0][1], sz);
+                        const float b1 = lerp(e[1][0], e[1][1], sz);
+                        const float b2 = lerp(e[2][0], e[2][1], sz);
+                        acc[z][0] += lerp(b0, b1, sx[0]);
+                        acc[z][1] += lerp(b0, b1, sx[1]);
+                        acc[z][2] += lerp(b1, b2, sx[2]);
+                        acc[z][3] += lerp(b1, b2, sx[3]);
+                    }
+                }
             }
+            continue;
         }
-        __syncthreads();
-        const float sy = S.ys[warp];
-        const int64_t iy = S.yi[warp];
+
+        // general octaves: per-voxel cell lookup (grid or hashed corners)
+        const bool direct = mode == kM3Direct;
         float sx[4];
         int64_t ixj[4];
+        float sy;
+        int64_t iy;
+        if (!direct) {
+            const Tab3& tb = S.tab[od.tslot];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            sx[j] = S.xs[c0 + j];
-            ixj[j] = S.xi[c0 + j];
+            for (int j = 0; j < 4; ++j) {
+                sx[j] = tb.xs[c0 + j];
+                ixj[j] = tb.xi[c0 + j];
+            }
+            sy = tb.ys[warp];
+            iy = tb.yi[warp];
+        } else {
+            float t;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                coord3(od, a.R, tx0 + c0 + j, &ixj[j], &t);
+                sx[j] = smooth3<ORDER>(t);
+            }
+            coord3(od, a.R, ty0 + warp, &iy, &t);
+            sy = smooth3<ORDER>(t);
         }
 #pragma unroll
         for (int z = 0; z < kTZ; ++z) {
-            const float sz = S.zs[z];
-            const int64_t iz = S.zi[z];
+            float sz;
+            int64_t iz;
+            if (!direct) {
+                sz = S.tab[od.tslot].zs[z];
+                iz = S.tab[od.tslot].zi[z];
+            } else {
+                float t;
+                coord3(od, a.R, tz0 + z, &iz, &t);
+                sz = smooth3<ORDER>(t);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 float h[8];
                 if (!direct) {
-                    const int b = (static_cast<int>(iz - iz0) * ncy + static_cast<int>(iy - iy0)) * ncx +
-                                  static_cast<int>(ixj[j] - ix0);
-                    h[0] = S.grid[b];
-                    h[1] = S.grid[b + 1];
-                    h[2] = S.grid[b + ncx];
-                    h[3] = S.grid[b + ncx + 1];
-                    h[4] = S.grid[b + ncx * ncy];
-                    h[5] = S.grid[b + ncx * ncy + 1];
-                    h[6] = S.grid[b + ncx * ncy + ncx];
-                    h[7] = S.grid[b + ncx * ncy + ncx + 1];
+                    const int b = static_cast<int>(iz) * plane + static_cast<int>(iy) * pitch + static_cast<int>(ixj[j]);
+                    const float* q = S.grid + od.goff + b;
+                    h[0] = q[0];
+                    h[1] = q[1];
+                    h[2] = q[pitch];
+                    h[3] = q[pitch + 1];
+                    h[4] = q[plane];
+                    h[5] = q[plane + 1];
+                    h[6] = q[plane + pitch];
+                    h[7] = q[plane + pitch + 1];
                 } else {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        h[q] = h3(base, ixj[j] + (q & 1), iy + ((q >> 1) & 1), iz + ((q >> 2) & 1), od.amp,
-                                  a.zero);
+                    for (int k = 0; k < 8; ++k)
+                        h[k] = height_scaled(pack3(base, ixj[j] + (k & 1), iy + ((k >> 1) & 1), iz + ((k >> 2) & 1)));
                 }
-                // x-lerped edges, then y, then z (multilinear in Sx, Sy, Sz)
                 const float b0 = lerp(lerp(h[0], h[2], sy), lerp(h[4], h[6], sy), sz);
                 const float b1 = lerp(lerp(h[1], h[3], sy), lerp(h[5], h[7], sy), sz);
-                acc[z][j] += lerp(b0, b1, sx[j]);
+                acc[z][j] = fmaf(amp, lerp(b0, b1, sx[j]), acc[z][j]);
             }
         }
     }
@@ -198,7 +395,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t lx = tx0 + c0 + j - a.ox;
-            if (lx >= 0 && lx < a.nx) row[lx] = acc[z][j];
+            if (lx >= 0 && lx < a.nx) row[lx] = acc[z][j] + racc[z];
         }
     }
 }
@@ -225,6 +422,61 @@ void fbm3d_tile(int* tx, int* ty, int* tz) {
     *tx = kTX;
     *ty = kTY;
     *tz = kTZ;
+}
+
+// Host plan for the 3D kernel: modes, corner-grid shapes and offsets.
+void fbm3d_plan(Fbm3Args* a, int zg_sep_only) {
+    (void)zg_sep_only;
+    int goff = 0, slot = 0;
+    for (int o = 0; o < a->octaves; ++o) {
+        OctDev& d = a->oct[o];
+        d.tslot = -1;
+        d.lut_off = -1;
+        if (d.cls == kClsSubInt) {
+            d.mode = kM3Sub;
+            continue;
+        }
+        int64_t nx, ny, nz;
+        int mode;
+        if (d.cls == kClsFast && d.shift >= 0 && d.shift <= kLutLog2Max) {
+            d.lut_off = (1 << d.shift) - 1;
+            nx = (d.ppc >= kTX ? 1 : kTX / d.ppc) + 1;
+            ny = (d.ppc >= kTY ? 1 : kTY / d.ppc) + 1;
+            nz = (d.ppc >= kTZ ? 1 : kTZ / d.ppc) + 1;
+            mode = d.ppc == 1 ? kM3P1 : kM3Blk;
+        } else {
+            double fx, fy, fz;
+            if (d.cls == kClsFast) {
+                fx = (kTX - 1) / d.ppc + 3;
+                fy = (kTY - 1) / d.ppc + 3;
+                fz = (kTZ - 1) / d.ppc + 3;
+            } else {
+                const double span = d.freq / a->R;
+                fx = std::ceil((kTX - 1) * span) + 3.0;
+                fy = std::ceil((kTY - 1) * span) + 3.0;
+                fz = std::ceil((kTZ - 1) * span) + 3.0;
+            }
+            nx = fx > 1e6 ? 1000000 : static_cast<int64_t>(fx);
+            ny = fy > 1e6 ? 1000000 : static_cast<int64_t>(fy);
+            nz = fz > 1e6 ? 1000000 : static_cast<int64_t>(fz);
+            mode = kM3Gen;
+        }
+        const int64_t pitch = (nx + 3) & ~int64_t(3);
+        const int64_t size = pitch * ny * nz;
+        if (nx * ny * nz > kCap3 || goff + size > kCap3 || (mode == kM3Gen && slot >= kTabs3)) {
+            d.mode = kM3Direct;
+            d.lut_off = -1;
+            continue;
+        }
+        d.mode = mode;
+        d.ncx = static_cast<int32_t>(nx);
+        d.ncy = static_cast<int32_t>(ny);
+        d.pad = static_cast<int32_t>(nz);
+        d.pitch = static_cast<int32_t>(pitch);
+        d.goff = goff;
+        goff += static_cast<int>(size);
+        if (mode == kM3Gen) d.tslot = slot++;
+    }
 }
 
 cudaError_t fbm3d_launch(int order, const Fbm3Args& a, float* out, cudaStream_t st) {

@@ -109,6 +109,7 @@ struct Fbm3Args {
     int32_t octaves;
     int32_t zero;
     uint64_t seed_key;
+    const float4* lut;  // row LUT (see FbmArgs)
     OctDev oct[kMaxOctaves];
 };
 

@@ -398,3 +398,15 @@ def test_device_band_stats_sum_to_whole_map(oracle):
         tot_coast += s.coast_pixels
     assert list(tot_c) == whole.counts and tot_coast == whole.coast_pixels
     assert np.array_equal(tot_pr, whole.pairs) and np.allclose(tot_ss, whole.sum_sq, rtol=1e-10)
+
+
+@pytest.mark.parametrize("R,f0,ratio,octs", [(60, 3, 2.0, 5), (48, 2, 1.7, 5), (64, 2, 2.0, 7)])
+def test_fbm3d_general_paths_match_oracle(oracle, R, f0, ratio, octs):
+    c = make_cfg(method=1, seed=2, resolution=R, base_frequency=f0, octaves=octs, frequency_ratio=ratio,
+                 smoothstep=5)
+    cfgp = pt.FbmConfig(method=1, seed=2, resolution=R, base_frequency=f0, octaves=octs, frequency_ratio=ratio,
+                        smoothstep=5)
+    n = min(R, 40)
+    out = torch.empty((n, n, n), dtype=torch.float32, device="cuda")
+    pt.generate3d_device(cfgp, (0, 0, 0), (n, n, n), out)
+    check_close(out.cpu().numpy(), oracle.generate3d(c, 0, 0, 0, n, n, n), c, f"3d R{R} f0{f0} r{ratio}")
