@@ -9,8 +9,10 @@ polynomial cell (zg_paper) with the quintic (C2) fade, 12 octaves,
 lacunarity 2, persistence 0.5, base cell 512 px (f0 = 8); octaves 10-11 are
 sub-pixel.  Synthetic by construction (no dataset: every sample is a pure
 function of the seed and pixel).  At N GPUs each rank generates its own
-4096^2 chunk of a 4096 x 4096N terrain with the same cell sizes (weak
-scaling, no data-path collective).
+config-2-sized 4096^2 chunk of a 32768^2 terrain with the same cell sizes
+(weak scaling, no data-path collective).  After the timed region the
+fractal-analysis pass (median sea level, coastline + box count, variogram)
+runs once on each rank's map with the statistics all-reduced (NCCL).
 
 Timing: W warm-up steps, then K steps back to back into 3 rotating output
 buffers (3 x 64 MiB = 192 MiB > 126 MB L2, so every step's writes reach HBM),
@@ -46,13 +48,71 @@ BYTES_PER_SAMPLE = 4         # one fp32 store per sample, no inputs
 def workload_cfg(world: int, rank: int):
     import paper_1610_03525_b200 as pt
 
-    # Weak scaling: R' = 4096*N with f0' = 8*N keeps every octave's pixels per
-    # cell (512 ... 1, then k = 2, 4) identical to config 2; rank r owns rows
-    # [r*4096, (r+1)*4096) x cols [0, 4096).
-    cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=R * world,
-                       base_frequency=F0 * world, octaves=OCTAVES, frequency_ratio=2.0,
+    if world == 1:
+        # config 2 exactly: a 4096^2 map, f0 = 8 (base cell 512 px)
+        cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=R,
+                           base_frequency=F0, octaves=OCTAVES, frequency_ratio=2.0,
+                           persistence=0.5, base_amplitude=1.0)
+        return cfg, (0, 0)
+    # Weak scaling: rank r generates its own 4096^2 chunk of a 32768^2 terrain
+    # with f0 = 64 (base cell 512 px): every octave has config 2's pixels per
+    # cell (512 ... 1, then lattice-point octaves k = 2, 4), so per-rank work is
+    # identical to config 2 for any N <= 64; no data-path collective.
+    T = 32768
+    cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=T,
+                       base_frequency=F0 * T // R, octaves=OCTAVES, frequency_ratio=2.0,
                        persistence=0.5, base_amplitude=1.0)
-    return cfg, (0, rank * R)
+    per_row = T // R
+    return cfg, ((rank % per_row) * R, (rank // per_row) * R)
+
+
+def analysis_pass(lib, ccfg, buf, stream_ptr, world, rank):
+    """Time the fractal-analysis pass on the step's map:
+    device radix-select median, fused coastline + box count, variogram over
+    lags 1..2048; statistics all-reduced across ranks (NCCL at N > 1)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_1610_03525_b200 import _abi
+    from paper_1610_03525_b200.shard import Comm, distributed_upper_median
+
+    comm = Comm(device=torch.device("cuda", torch.cuda.current_device()))
+    sizes = [2, 4, 8, 16, 32, 64]
+    lags = [1 << i for i in range(12)]
+
+    def hist(prefix, mask, shift, bits):
+        out = np.zeros(1 << bits, dtype=np.uint64)
+        assert lib.tg_histogram_f32(buf.data_ptr(), R, R, R, prefix, mask, shift, bits, out.ctypes.data,
+                                    stream_ptr) == 0, _abi.last_error()
+        return out.astype(np.int64)
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sea = distributed_upper_median(hist, R * R * world, comm)
+    arr = (C.c_int32 * 6)(*sizes)
+    cnt = (C.c_int64 * 6)()
+    coast, land = C.c_int64(), C.c_int64()
+    assert lib.tg_coastline_boxcount_band(buf.data_ptr(), R, R, R, 0, 0, sea, arr, 6, cnt, C.byref(coast),
+                                          C.byref(land), stream_ptr) == 0, _abi.last_error()
+    t1 = time.perf_counter()
+    la = (C.c_int32 * len(lags))(*lags)
+    ss = (C.c_double * (2 * len(lags)))()
+    pr = (C.c_int64 * (2 * len(lags)))()
+    assert lib.tg_variogram_f32(buf.data_ptr(), R, R, R, la, len(lags), ss, pr, stream_ptr) == 0, _abi.last_error()
+    t2 = time.perf_counter()
+    red = comm.allreduce(np.array(list(cnt) + [coast.value, land.value], dtype=np.int64))
+    ssr = comm.allreduce(np.array(ss[:]))
+    t3 = time.perf_counter()
+    counts = [int(v) for v in red[:6]]
+    lx = [math.log(s) for s in sizes]
+    ly = [math.log(max(c, 1)) for c in counts]
+    mx, my = sum(lx) / 6, sum(ly) / 6
+    slope = sum((a - mx) * (b - my) for a, b in zip(lx, ly)) / sum((a - mx) ** 2 for a in lx)
+    return {"median_coast_boxcount_ms": (t1 - t0) * 1e3, "variogram_ms": (t2 - t1) * 1e3,
+            "allreduce_ms": (t3 - t2) * 1e3, "sea_level": sea, "box_counts": counts, "d_box": -slope,
+            "note": "per-rank 4096^2 map; host wall clock incl. syncs; statistics all-reduced over ranks"}
 
 
 class ClockSampler:
@@ -181,6 +241,7 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-analysis", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -246,22 +307,32 @@ def main() -> None:
     hbm_gbs = BYTES_PER_SAMPLE * R * R / avg_launch_s / 1e9
 
     # ---- end to end through the drop-in host API (generate_into(span<double>)) ----
-    e2e_steps = args.e2e_steps or max(3, min(K, 20))
+    e2e_steps = args.e2e_steps or max(5, min(K, 20))
     host = torch.empty((R, R), dtype=torch.float64, pin_memory=True)
-    for _ in range(2):
+    for _ in range(3):
         st = lib.tg_fbm_generate_f64_host(C.byref(ccfg), origin[0], origin[1], R, host.data_ptr(), R * R)
         assert st == 0, _abi.last_error()
     if world > 1:
         dist.barrier()
+    e2e_each = []
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
+        t1 = time.perf_counter()
         st = lib.tg_fbm_generate_f64_host(C.byref(ccfg), origin[0], origin[1], R, host.data_ptr(), R * R)
         assert st == 0, _abi.last_error()
+        e2e_each.append(time.perf_counter() - t1)
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = so_per_step * e2e_steps * world / float(te.item())
+
+    analysis = None
+    if not args.no_analysis:
+        try:
+            analysis = analysis_pass(lib, ccfg, bufs[(K - 1) % 3], sp, world, rank)
+        except Exception as e:  # pragma: no cover
+            analysis = {"error": str(e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -281,9 +352,10 @@ def main() -> None:
             "warmup": max(args.warmup, 3), "ms_per_step": total_ms_max / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"config 2: {R}x{R} fp32 fBm, zg_paper C2 (S5), {OCTAVES} octaves, "
-                                   f"lacunarity 2, persistence 0.5, base cell 512 px",
+                                   f"lacunarity 2, persistence 0.5, base cell 512 px"
+                                   + ("" if world == 1 else f"; one such chunk per rank of a 32768^2 terrain"),
                        "global_maps_per_step": world, "samples_per_step_per_gpu": R * R,
-                       "parallelism": f"shard{world} (row-band chunks, no data-path collective)",
+                       "parallelism": f"shard{world} (independent chunks, no data-path collective)",
                        "l2": "3 rotating 64 MiB outputs (192 MiB > 126 MB L2)"},
             "roofline": {"bound": "fp32", "achieved": achieved_tflops, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
@@ -294,12 +366,15 @@ def main() -> None:
                                   f"(MEASURED_PEAKS.json has no FP32 entry)"),
                          "hbm_write_gbs": hbm_gbs, "hbm_frac": hbm_gbs / 6458.4},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(ccfg),
-                    "d2h_bytes_per_step": R * R * 8,
+                    "d2h_bytes_per_step": R * R * 8, "steps": e2e_steps,
+                    "ms_per_step_median": statistics.median(e2e_each) * 1e3,
+                    "d2h_gbs": R * R * 8 / statistics.median(e2e_each) / 1e9,
                     "note": "tg_fbm_generate_f64_host (drop-in generate_into span<double>) into pinned host "
                             "memory; input is the config struct only"},
             "gpu_launches": K,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "analysis": analysis,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
