@@ -35,27 +35,49 @@ struct SelectState {
 
 constexpr int kBins = 2048;
 
+// Per-block shared-memory histograms written to partials[block][bin] (no
+// global atomics), summed by hist_reduce: 2048 bins x a few hundred blocks of
+// global atomics on 2048 addresses would serialise in L2.
+constexpr int kHistBlocks = 296;
+
 __global__ void radix_hist(const float* __restrict__ x, uint64_t n, const SelectState* st,
-                           int shift, int bits, unsigned long long* __restrict__ hist) {
+                           int shift, int bits, unsigned int* __restrict__ partials) {
     __shared__ unsigned int sh[kBins];
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const uint32_t prefix = st->prefix, mask = st->mask;
     const uint32_t dmask = (1u << bits) - 1u;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t n4 = (reinterpret_cast<uintptr_t>(x) & 15) == 0 ? n / 4 : 0;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+        const float4 v = x4[i];
+        const uint32_t k[4] = {fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w)};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if ((k[u] & mask) == prefix) atomicAdd(&sh[(k[u] >> shift) & dmask], 1u);
+    }
+    for (uint64_t i = n4 * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
         const uint32_t key = fkey(x[i]);
         if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & dmask], 1u);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
-        if (sh[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(sh[i]));
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) partials[blockIdx.x * kBins + i] = sh[i];
+}
+
+__global__ void hist_reduce(const unsigned int* __restrict__ partials, int blocks,
+                            unsigned long long* __restrict__ hist) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= kBins) return;
+    unsigned long long s = 0;
+    for (int k = 0; k < blocks; ++k) s += partials[k * kBins + b];
+    hist[b] = s;
 }
 
 // Strided-window form (row bands with halos): blocks stride over rows.
 __global__ void radix_hist2d(const float* __restrict__ x, int64_t width, int64_t rows, int64_t ld,
                              const SelectState* st, int shift, int bits,
-                             unsigned long long* __restrict__ hist) {
+                             unsigned int* __restrict__ partials) {
     __shared__ unsigned int sh[kBins];
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -67,8 +89,7 @@ __global__ void radix_hist2d(const float* __restrict__ x, int64_t width, int64_t
             if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & dmask], 1u);
         }
     __syncthreads();
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
-        if (sh[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(sh[i]));
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) partials[blockIdx.x * kBins + i] = sh[i];
 }
 
 __global__ void radix_pick(SelectState* st, unsigned long long* hist, int shift, int bits) {
@@ -283,16 +304,18 @@ int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* str
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Scratch scr(s);
-    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long));
+    const size_t part_bytes = static_cast<size_t>(kHistBlocks) * kBins * sizeof(unsigned int);
+    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long) + part_bytes);
     if (e != cudaSuccess) return set_cuda_error(e, "median alloc");
     SelectState* state = static_cast<SelectState*>(scr.p);
     unsigned long long* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);
+    unsigned int* partials = reinterpret_cast<unsigned int*>(hist + kBins);
     SelectState init{0u, 0u, n / 2};  // analysis.hpp:247 (upper median)
     e = cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned long long), s);
     const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
     for (int p = 0; p < 3 && e == cudaSuccess; ++p) {
-        radix_hist<<<148 * 4, 512, 0, s>>>(dev_map, n, state, shifts[p], widths[p], hist);
+        radix_hist<<<kHistBlocks, 512, 0, s>>>(dev_map, n, state, shifts[p], widths[p], partials);
+        hist_reduce<<<kBins / 256, 256, 0, s>>>(partials, kHistBlocks, hist);
         radix_pick<<<1, 32, 0, s>>>(state, hist, shifts[p], widths[p]);
         e = cudaGetLastError();
     }
@@ -499,16 +522,22 @@ int tg_histogram_f32(const float* dev_rows, int64_t width, int64_t rows, int64_t
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Scratch scr(s);
-    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long));
+    const size_t part_bytes = static_cast<size_t>(kHistBlocks) * kBins * sizeof(unsigned int);
+    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long) + part_bytes);
     if (e != cudaSuccess) return set_cuda_error(e, "histogram alloc");
     SelectState* state = static_cast<SelectState*>(scr.p);
     auto* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);
+    unsigned int* partials = reinterpret_cast<unsigned int*>(hist + kBins);
     SelectState init{prefix, mask, 0};
     e = cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned long long), s);
+    const int blocks = static_cast<int>(std::min<int64_t>(rows, kHistBlocks));
     if (e == cudaSuccess) {
-        radix_hist2d<<<static_cast<unsigned>(std::min<int64_t>(rows, 148 * 4)), 512, 0, s>>>(
-            dev_rows, width, rows, ld, state, shift, bits, hist);
+        if (ld == width)
+            radix_hist<<<kHistBlocks, 512, 0, s>>>(dev_rows, static_cast<uint64_t>(width * rows), state, shift, bits,
+                                                   partials);
+        else
+            radix_hist2d<<<blocks, 512, 0, s>>>(dev_rows, width, rows, ld, state, shift, bits, partials);
+        hist_reduce<<<kBins / 256, 256, 0, s>>>(partials, ld == width ? kHistBlocks : blocks, hist);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess)

@@ -9,6 +9,7 @@
 // Errors map onto terrain/errors.hpp through the tg_status codes.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -225,6 +226,21 @@ int validate_window(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t widt
     return TG_OK;
 }
 
+// Scratch buffers come from the device's default stream-ordered pool; keep
+// freed blocks cached in the pool (default release threshold 0 would unmap
+// them at every synchronisation and remap on the next call).
+void keep_pool(int dev) {
+    static std::atomic<uint64_t> done{0};
+    if (dev < 0 || dev >= 64 || (done.load() >> dev) & 1ULL) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done.fetch_or(1ULL << dev);
+}
+
 int device_ready() {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
@@ -232,6 +248,8 @@ int device_ready() {
         cudaGetLastError();
         return fail(TG_EDEVICE, "no CUDA device: the B200 path has no CPU fallback");
     }
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) keep_pool(dev);
     return TG_OK;
 }
 
