@@ -167,6 +167,14 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": rs, "samples": len(self.samples)}
 
 
+def traffic_summary():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def traffic_from_profiles():
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
@@ -364,7 +372,11 @@ def main() -> None:
                                   f"x {int(so_per_step)} sample-octaves per launch / mean CUDA-event launch "
                                   f"time {avg_launch_s*1e6:.1f} us; peak = FFMA-chain measured in-run "
                                   f"(MEASURED_PEAKS.json has no FP32 entry)"),
-                         "hbm_write_gbs": hbm_gbs, "hbm_frac": hbm_gbs / 6458.4},
+                         "hbm_write_gbs": hbm_gbs, "hbm_frac": hbm_gbs / 6458.4,
+                         "issue_slots_busy_pct_ncu": (traffic_summary() or {}).get("issue_active_pct"),
+                         "issue_note": "the bit-exact 64-bit lattice hash is integer work outside the 7-flop "
+                                       "convention; issue-slot utilisation of the same kernel from the committed "
+                                       "ncu capture (profiles/ncu_summary.json)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(ccfg),
                     "d2h_bytes_per_step": R * R * 8, "steps": e2e_steps,
                     "ms_per_step_median": statistics.median(e2e_each) * 1e3,
