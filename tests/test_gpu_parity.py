@@ -410,3 +410,39 @@ def test_fbm3d_general_paths_match_oracle(oracle, R, f0, ratio, octs):
     out = torch.empty((n, n, n), dtype=torch.float32, device="cuda")
     pt.generate3d_device(cfgp, (0, 0, 0), (n, n, n), out)
     check_close(out.cpu().numpy(), oracle.generate3d(c, 0, 0, 0, n, n, n), c, f"3d R{R} f0{f0} r{ratio}")
+
+
+# ---- edge cases: extreme origins / octave counts / odd resolutions -------------------
+
+@pytest.mark.parametrize("method", [0, 2, 3])
+def test_far_origin_near_limit(oracle, method):
+    # |origin| up to 2^40 (fbm.hpp:552); lattice indices then need full int64 keys
+    R = 1024
+    for ox, oy in [((1 << 40) - 1024, -(1 << 40)), (-(1 << 39), (1 << 39) + 512)]:
+        c = make_cfg(method=method, seed=2**64 - 7, resolution=R, base_frequency=2, octaves=10)
+        m = gen(c, ox, oy, 96, 64)
+        ys, xs = np.meshgrid(np.arange(oy, oy + 64), np.arange(ox, ox + 96), indexing="ij")
+        ref = oracle.sample(c, xs.ravel(), ys.ravel()).reshape(64, 96)
+        check_close(m.cpu().numpy(), ref, c, f"far origin m{method}")
+
+
+def test_thirty_two_octaves(oracle):
+    c = make_cfg(method=0, smoothstep=5, seed=9, resolution=1024, base_frequency=1, octaves=32, persistence=0.9)
+    m = gen(c, 0, 0, 128)
+    check_close(m.cpu().numpy(), oracle.generate(c, 0, 0, 128), c, "32 octaves")
+
+
+@pytest.mark.parametrize("R,f0", [(1000, 8), (768, 3), (4097, 1)])
+def test_odd_resolutions(oracle, R, f0):
+    for method in (0, 3):
+        c = make_cfg(method=method, seed=4, resolution=R, base_frequency=f0, octaves=9)
+        m = gen(c, 0, 0, 256)
+        check_close(m.cpu().numpy(), oracle.generate(c, 0, 0, 256), c, f"R{R} f0{f0} m{method}")
+
+
+@pytest.mark.parametrize("method", [1, 2, 4])
+def test_s5_other_methods(oracle, method):
+    c = make_cfg(method=method, smoothstep=5, seed=12, resolution=2048, base_frequency=4, octaves=11)
+    m = gen(c, 0, 0, 2048)
+    check_close(m[:128, :128].cpu().numpy(), oracle.generate(c, 0, 0, 128), c, f"S5 m{method}")
+    _sample_check(oracle, c, m, 0, 0, n=2048)
