@@ -38,13 +38,19 @@ enum tg_status {
     TG_EDEVICE = 4
 };
 
-/* terrain::fbm::Method, same order (fbm.hpp:27). */
+/* terrain::fbm::Method, same order (fbm.hpp:27), plus the paper's third
+ * comparison baseline that the reference does not implement:
+ * OpenSimplex 2D (2014 geometry: stretch/squish skew, 3 + 1 vertex
+ * contributions with (2 - d^2)^4 falloff, 8 gradients, /47) with gradients
+ * chosen by the lattice hash instead of a permutation table.  New; parity
+ * unpinned (restated oracle only). */
 enum tg_method {
     TG_METHOD_ZG_PAPER = 0,
     TG_METHOD_ZG_SEPARABLE = 1,
     TG_METHOD_GENERIC = 2,
     TG_METHOD_PERLIN3 = 3,
-    TG_METHOD_PERLIN5 = 4
+    TG_METHOD_PERLIN5 = 4,
+    TG_METHOD_OPENSIMPLEX = 5
 };
 
 /* Lifted caps: the reference caps resolution and extent at
@@ -57,6 +63,8 @@ enum tg_method {
 #define TG_LANE_HEIGHT 0ULL
 #define TG_LANE_ANGLE 0xA0761D6478BD642FULL
 #define TG_LANE_MAGNITUDE 0xE7037ED1A0B428DBULL
+/* OpenSimplex gradient-selection lane (new): index = mix(pack ^ lane) >> 61. */
+#define TG_LANE_SIMPLEX 0x8EBC6AF09C88C6E3ULL
 /* 3D key extension (new): pack3 = pack2 + (u64)iz * K5,
  * so iz = 0 reproduces the 2D lattice exactly. */
 #define TG_PACK_K5 0xA24BAED4963EE407ULL

@@ -63,7 +63,9 @@ inline void check(int status) {
 
 namespace fbm {
 
-enum class Method { zg_paper, zg_separable, generic, perlin3, perlin5 };  // fbm.hpp:27
+// fbm.hpp:27, plus opensimplex (the paper's third baseline; absent from the
+// reference)
+enum class Method { zg_paper, zg_separable, generic, perlin3, perlin5, opensimplex };
 
 inline const char* method_name(Method m) {  // fbm.hpp:29-38
     switch (m) {
@@ -72,6 +74,7 @@ inline const char* method_name(Method m) {  // fbm.hpp:29-38
         case Method::generic: return "generic";
         case Method::perlin3: return "perlin3";
         case Method::perlin5: return "perlin5";
+        case Method::opensimplex: return "opensimplex";
     }
     return "unknown";
 }
@@ -82,6 +85,7 @@ inline std::optional<Method> parse_method(std::string_view name) {  // fbm.hpp:4
     if (name == "generic") return Method::generic;
     if (name == "perlin3" || name == "perlin") return Method::perlin3;
     if (name == "perlin5") return Method::perlin5;
+    if (name == "opensimplex") return Method::opensimplex;
     return std::nullopt;
 }
 

@@ -148,6 +148,70 @@ double or_perlin_eval(const double f[4], const double g[4], int order, double x,
     return h0 + sy * (h1 - h0);
 }
 
+/* OpenSimplex 2D (new, parity unpinned): the 2014 OpenSimplex
+ * geometry restated from its published description — stretch the input onto
+ * a skewed square lattice, locate the rhombus and its triangle, sum
+ * (2 - d^2)^4 * (g . d) over the two fixed vertices, the closest corner and
+ * one extra vertex, divide by 47.  Gradients: the 8 vectors (+-5, +-2),
+ * (+-2, +-5), chosen by the lattice hash (lane TG_LANE_SIMPLEX). */
+#define OS_STRETCH (-0.211324865405187117745425609749)
+#define OS_SQUISH 0.366025403784438646763723170753
+static const double OS_GRAD[16] = {5, 2, 2, 5, -5, 2, -2, 5, 5, -2, 2, -5, -5, -2, -2, -5};
+
+static double os_contrib(uint64_t seed, uint32_t oct, int64_t xsv, int64_t ysv, double dx, double dy) {
+    double attn = 2.0 - dx * dx - dy * dy;
+    if (attn <= 0.0) return 0.0;
+    const int gi = (int)(or_hash(seed, oct, xsv, ysv, TG_LANE_SIMPLEX) >> 61) * 2;
+    attn *= attn;
+    return attn * attn * (OS_GRAD[gi] * dx + OS_GRAD[gi + 1] * dy);
+}
+
+double or_opensimplex(uint64_t seed, uint32_t oct, double x, double y) {
+    const double so = (x + y) * OS_STRETCH;
+    const double xs = x + so, ys = y + so;
+    int64_t xsb = (int64_t)floor(xs), ysb = (int64_t)floor(ys);
+    const double sq = (double)(xsb + ysb) * OS_SQUISH;
+    const double xins = xs - (double)xsb, yins = ys - (double)ysb;
+    const double in_sum = xins + yins;
+    double dx0 = x - ((double)xsb + sq), dy0 = y - ((double)ysb + sq);
+    double v = 0.0;
+    /* the two vertices (1,0) and (0,1) of the rhombus */
+    v += os_contrib(seed, oct, xsb + 1, ysb, dx0 - 1.0 - OS_SQUISH, dy0 - OS_SQUISH);
+    v += os_contrib(seed, oct, xsb, ysb + 1, dx0 - OS_SQUISH, dy0 - 1.0 - OS_SQUISH);
+    int64_t xe, ye;
+    double dxe, dye;
+    if (in_sum <= 1.0) { /* triangle (0,0), (1,0), (0,1) */
+        const double zins = 1.0 - in_sum;
+        if (zins > xins || zins > yins) {
+            if (xins > yins) {
+                xe = xsb + 1; ye = ysb - 1; dxe = dx0 - 1.0; dye = dy0 + 1.0;
+            } else {
+                xe = xsb - 1; ye = ysb + 1; dxe = dx0 + 1.0; dye = dy0 - 1.0;
+            }
+        } else {
+            xe = xsb + 1; ye = ysb + 1; dxe = dx0 - 1.0 - 2.0 * OS_SQUISH; dye = dy0 - 1.0 - 2.0 * OS_SQUISH;
+        }
+    } else { /* triangle (1,0), (0,1), (1,1) */
+        const double zins = 2.0 - in_sum;
+        if (zins < xins || zins < yins) {
+            if (xins > yins) {
+                xe = xsb + 2; ye = ysb; dxe = dx0 - 2.0 - 2.0 * OS_SQUISH; dye = dy0 - 2.0 * OS_SQUISH;
+            } else {
+                xe = xsb; ye = ysb + 2; dxe = dx0 - 2.0 * OS_SQUISH; dye = dy0 - 2.0 - 2.0 * OS_SQUISH;
+            }
+        } else {
+            xe = xsb; ye = ysb; dxe = dx0; dye = dy0;
+        }
+        xsb += 1;
+        ysb += 1;
+        dx0 = dx0 - 1.0 - 2.0 * OS_SQUISH;
+        dy0 = dy0 - 1.0 - 2.0 * OS_SQUISH;
+    }
+    v += os_contrib(seed, oct, xsb, ysb, dx0, dy0); /* (0,0) or (1,1) */
+    v += os_contrib(seed, oct, xe, ye, dxe, dye);   /* extra vertex */
+    return v / 47.0;
+}
+
 /* FbmConfig::validate (fbm.hpp:71-88) with the lifted caps. */
 int or_validate(const tg_fbm_config* c) {
     if (c->octaves < 1 || c->octaves > TG_MAX_OCTAVES) return TG_EVALIDATION;
@@ -159,7 +223,7 @@ int or_validate(const tg_fbm_config* c) {
     if (c->has_gradient_weight && (!(c->gradient_weight >= 0.0) || !isfinite(c->gradient_weight)))
         return TG_EVALIDATION;
     if (c->threads < 0 || c->threads > 256) return TG_EVALIDATION;
-    if (c->method < 0 || c->method > 4) return TG_EVALIDATION;
+    if (c->method < 0 || c->method > TG_METHOD_OPENSIMPLEX) return TG_EVALIDATION;
     if (c->smoothstep != 0 && c->smoothstep != 3 && c->smoothstep != 5) return TG_EVALIDATION;
     return TG_OK;
 }
@@ -285,6 +349,11 @@ static double fast_sample(const tg_fbm_config* c, int oct, const tg_octave_spec*
 static double general_sample(const tg_fbm_config* c, int oct, const tg_octave_spec* os,
                              int64_t gx, int64_t gy, int order) {
     const double R = (double)c->resolution;
+    if (c->method == TG_METHOD_OPENSIMPLEX) { /* continuous sample position, every octave */
+        if (c->zero_lattice) return 0.0;
+        const double u = ((double)gx + 0.5) / R * os->freq, v = ((double)gy + 0.5) / R * os->freq;
+        return os->amp * or_opensimplex(c->seed, (uint32_t)oct, u, v);
+    }
     const double v = ((double)gy + 0.5) / R * os->freq;
     const int64_t iy = (int64_t)floor(v);
     const double cy = v - (double)iy;
@@ -348,8 +417,9 @@ int or_generate(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, i
         for (int64_t ly = 0; ly < height; ++ly) {
             double* row = out + (size_t)ly * (size_t)width;
             for (int64_t lx = 0; lx < width; ++lx) {
-                const double v = os.fast ? fast_sample(c, oct, &os, ox + lx, oy + ly, order)
-                                         : general_sample(c, oct, &os, ox + lx, oy + ly, order);
+                const double v = os.fast && c->method != TG_METHOD_OPENSIMPLEX
+                                     ? fast_sample(c, oct, &os, ox + lx, oy + ly, order)
+                                     : general_sample(c, oct, &os, ox + lx, oy + ly, order);
                 row[lx] += v;
             }
         }
@@ -369,8 +439,9 @@ int or_sample(const tg_fbm_config* c, const int64_t* gx, const int64_t* gy, int6
         tg_octave_spec os;
         or_octave_spec(c, oct, &os);
         for (int64_t i = 0; i < n; ++i)
-            out[i] += os.fast ? fast_sample(c, oct, &os, gx[i], gy[i], order)
-                              : general_sample(c, oct, &os, gx[i], gy[i], order);
+            out[i] += os.fast && c->method != TG_METHOD_OPENSIMPLEX
+                          ? fast_sample(c, oct, &os, gx[i], gy[i], order)
+                          : general_sample(c, oct, &os, gx[i], gy[i], order);
     }
     return TG_OK;
 }

@@ -20,6 +20,7 @@ TG_METHOD_ZG_SEPARABLE = 1
 TG_METHOD_GENERIC = 2
 TG_METHOD_PERLIN3 = 3
 TG_METHOD_PERLIN5 = 4
+TG_METHOD_OPENSIMPLEX = 5
 
 TG_MAX_RESOLUTION = 1 << 22
 TG_MAX_EXTENT = 1 << 17
@@ -28,6 +29,7 @@ TG_MAX_OCTAVES = 32
 TG_LANE_HEIGHT = 0
 TG_LANE_ANGLE = 0xA0761D6478BD642F
 TG_LANE_MAGNITUDE = 0xE7037ED1A0B428DB
+TG_LANE_SIMPLEX = 0x8EBC6AF09C88C6E3
 TG_PACK_K5 = 0xA24BAED4963EE407
 
 

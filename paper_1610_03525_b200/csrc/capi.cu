@@ -68,6 +68,7 @@ int kind_of(const tg_fbm_config* c) {
         case TG_METHOD_ZG_PAPER: return tg::kZgPaper;
         case TG_METHOD_ZG_SEPARABLE: return tg::kZgSeparable;
         case TG_METHOD_GENERIC: return tg::kGeneric;
+        case TG_METHOD_OPENSIMPLEX: return tg::kOpenSimplex;
         default: return tg::kPerlin;
     }
 }
@@ -204,7 +205,7 @@ int validate_cfg(const tg_fbm_config* c) {
         return fail(TG_EVALIDATION, "fbm config: gradient_weight must be non-negative");
     if (c->threads < 0 || c->threads > 256)
         return fail(TG_EVALIDATION, "fbm config: threads must be in [0, 256]");
-    if (c->method < TG_METHOD_ZG_PAPER || c->method > TG_METHOD_PERLIN5)
+    if (c->method < TG_METHOD_ZG_PAPER || c->method > TG_METHOD_OPENSIMPLEX)
         return fail(TG_EVALIDATION, "fbm config: unknown method");
     if (c->smoothstep != 0 && c->smoothstep != 3 && c->smoothstep != 5)
         return fail(TG_EVALIDATION, "fbm config: smoothstep must be 0, 3 or 5");

@@ -57,6 +57,7 @@ class Method(enum.IntEnum):
     generic = 2
     perlin3 = 3
     perlin5 = 4
+    opensimplex = 5  # B200 extension: the paper's third baseline (parity unpinned)
 
 
 def method_name(m: Method) -> str:  # fbm.hpp:29-38
@@ -67,7 +68,7 @@ def parse_method(name: str) -> Optional[Method]:  # fbm.hpp:40-47
     return {"zg_paper": Method.zg_paper, "zg": Method.zg_paper,
             "zg_separable": Method.zg_separable, "generic": Method.generic,
             "perlin3": Method.perlin3, "perlin": Method.perlin3,
-            "perlin5": Method.perlin5}.get(name)
+            "perlin5": Method.perlin5, "opensimplex": Method.opensimplex}.get(name)
 
 
 @dataclass

@@ -446,3 +446,20 @@ def test_s5_other_methods(oracle, method):
     m = gen(c, 0, 0, 2048)
     check_close(m[:128, :128].cpu().numpy(), oracle.generate(c, 0, 0, 128), c, f"S5 m{method}")
     _sample_check(oracle, c, m, 0, 0, n=2048)
+
+
+# ---- OpenSimplex (new baseline; parity vs the restated oracle, unpinned) ------------
+
+@pytest.mark.parametrize("R,f0,octs,ratio", [(256, 2, 6, 2.0), (4096, 8, 12, 2.0), (100, 3, 5, 1.7)])
+def test_opensimplex_matches_restated_oracle(oracle, R, f0, octs, ratio):
+    c = make_cfg(method=5, seed=77, resolution=R, base_frequency=f0, octaves=octs, frequency_ratio=ratio)
+    n = min(R, 256)
+    m = gen(c, 0, 0, n)
+    check_close(m.cpu().numpy(), oracle.generate(c, 0, 0, n), c, f"opensimplex R{R}")
+
+
+def test_opensimplex_region_and_zero():
+    c = make_cfg(method=5, seed=909, resolution=64, octaves=3)
+    assert torch.equal(gen(c, 32, 32, 32), gen(c, 0, 0, 64)[32:, 32:])
+    c.zero_lattice = 1
+    assert torch.count_nonzero(gen(c, 0, 0, 64)).item() == 0
