@@ -351,7 +351,8 @@ static double general_sample(const tg_fbm_config* c, int oct, const tg_octave_sp
     const double R = (double)c->resolution;
     if (c->method == TG_METHOD_OPENSIMPLEX) { /* continuous sample position, every octave */
         if (c->zero_lattice) return 0.0;
-        const double u = ((double)gx + 0.5) / R * os->freq, v = ((double)gy + 0.5) / R * os->freq;
+        const double fr = os->freq / R; /* same operation order as the CUDA kernel */
+        const double u = ((double)gx + 0.5) * fr, v = ((double)gy + 0.5) * fr;
         return os->amp * or_opensimplex(c->seed, (uint32_t)oct, u, v);
     }
     const double v = ((double)gy + 0.5) / R * os->freq;

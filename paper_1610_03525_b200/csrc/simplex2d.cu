@@ -8,7 +8,8 @@
 // triangle's own corner and one extra vertex, divide by 47.  Gradients are
 // the 8 vectors (+-5, +-2), (+-2, +-5) chosen by the lattice hash (lane
 // TG_LANE_SIMPLEX), so chunks stay stateless like every other method.  Sample
-// positions follow render_general: u = ((g + 0.5)/R) * freq (fbm.hpp:468).
+// positions are u = (g + 0.5) * (freq / R) (render_general's position,
+// fbm.hpp:468, with the ratio formed once per octave).
 // Skew, floor and region decisions run in fp64 (as the oracle), the four
 // contributions in fp32.  256 threads x 4 x 8 pixels, one fp32 store.
 #include <cuda_runtime.h>
@@ -104,8 +105,9 @@ simplex2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) 
         float acc = 0.f;
         for (int o = 0; o < args.octaves; ++o) {
             const OctDev& od = args.oct[o];
-            const double u = __dmul_rn(__ddiv_rn(__dadd_rn(gx, 0.5), args.R), od.freq);
-            const double v = __dmul_rn(__ddiv_rn(__dadd_rn(gy, 0.5), args.R), od.freq);
+            const double fr = __ddiv_rn(od.freq, args.R);  // uniform: hoisted by the compiler
+            const double u = __dmul_rn(__dadd_rn(gx, 0.5), fr);
+            const double v = __dmul_rn(__dadd_rn(gy, 0.5), fr);
             acc = fmaf(od.amp, opensimplex(seed_key + od.oct_key, u, v), acc);
         }
         const int64_t ly = ly0 + r, lx = lx0 + j;
