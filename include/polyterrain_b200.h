@@ -176,6 +176,14 @@ int tg_minmax_f32(const float* dev_map, uint64_t n, double* out_min, double* out
 /* In-place affine rescale to [-1, 1] with the given source range. */
 int tg_rescale_f32(float* dev_map, uint64_t n, double lo, double hi, void* stream);
 
+/* quantize16 (io.hpp:61-65) of a device map into the byte layout of a 16-bit
+ * PGM body (big-endian samples) or, with png_rows != 0, of the PNG raw image
+ * (filter byte 0 + big-endian samples per row, io.hpp:228-239); dev_out holds
+ * height * (2*width [+1]) bytes.  lo/hi: the map's range (tg_minmax_f32).
+ * Stream-ordered; the caller writes the header / zlib-compresses on the host. */
+int tg_pack16_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld, double lo,
+                  double hi, int32_t png_rows, uint8_t* dev_out, void* stream);
+
 /* ---- fractal analysis (analysis.hpp:213-305; variogram new) --------------- */
 
 /* Upper median (element n/2 of the sorted map, analysis.hpp:244-250) by

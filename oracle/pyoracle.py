@@ -219,6 +219,8 @@ class Reference:
             "ref_box_count_mask": (C.c_int, [P, I32, P, I32, P, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
             "ref_linear_fit": (C.c_int, [P, P, I32, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
             "ref_run_bench": (C.c_int, [PCFG, I32, I32, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
+            "ref_encode_pgm16": (I64, [P, I32, I32, P, I64]),
+            "ref_encode_png16": (I64, [P, I32, I32, P, I64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -312,6 +314,17 @@ class Reference:
         st = self.lib.ref_box_count_mask(_ptr(m), m.shape[0], _ptr(sz), len(sz), _ptr(counts),
                                          C.byref(d), C.byref(k), C.byref(r2))
         return st, counts, d.value, k.value, r2.value
+
+    def encode16(self, data: np.ndarray, png: bool) -> bytes:
+        d = np.ascontiguousarray(data, dtype=np.float64)
+        h, w = d.shape
+        cap = 2 * d.size + h + 4096
+        buf = np.zeros(cap, dtype=np.uint8)
+        fn = self.lib.ref_encode_png16 if png else self.lib.ref_encode_pgm16
+        n = fn(_ptr(d), w, h, _ptr(buf), cap)
+        if n < 0:
+            raise ValueError(self.last_error())
+        return buf[:n].tobytes()
 
     def run_bench(self, cfg, reps: int, warmup: int):
         med, mn, mean = F64(), F64(), F64()

@@ -11,12 +11,14 @@
 #include <cstring>
 #include <exception>
 #include <span>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "terrain/analysis.hpp"
 #include "terrain/bench.hpp"
 #include "terrain/fbm.hpp"
+#include "terrain/io.hpp"
 #include "terrain/kernels2d.hpp"
 #include "terrain/lattice.hpp"
 
@@ -305,6 +307,36 @@ int ref_box_count_mask(const uint8_t* mask, int32_t R, const int32_t* sizes, int
         *k = rep.k;
         *r2 = rep.r2;
     });
+}
+
+// write_pgm16 / write_png16 (io.hpp:91-111, 203-257) into a caller buffer;
+// returns the byte count (or -1 when it does not fit / on error).
+static int64_t put_bytes(const std::string& b, uint8_t* out, int64_t cap) {
+    if (static_cast<int64_t>(b.size()) > cap) return -1;
+    std::memcpy(out, b.data(), b.size());
+    return static_cast<int64_t>(b.size());
+}
+
+int64_t ref_encode_pgm16(const double* data, int32_t width, int32_t height, uint8_t* out, int64_t cap) {
+    try {
+        std::ostringstream os;
+        io::write_pgm16(os, std::span<const double>(data, static_cast<size_t>(width) * height), width, height);
+        return put_bytes(os.str(), out, cap);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int64_t ref_encode_png16(const double* data, int32_t width, int32_t height, uint8_t* out, int64_t cap) {
+    try {
+        std::ostringstream os;
+        io::write_png16(os, std::span<const double>(data, static_cast<size_t>(width) * height), width, height);
+        return put_bytes(os.str(), out, cap);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
 }
 
 // linear_fit (analysis.hpp:29-63).

@@ -102,6 +102,7 @@ SIGNATURES = {
     "tg_lattice_unit_gradient_f32": (C.c_int, [P, U64, P, P]),
     "tg_minmax_f32": (C.c_int, [P, U64, C.POINTER(F64), C.POINTER(F64), P]),
     "tg_rescale_f32": (C.c_int, [P, U64, F64, F64, P]),
+    "tg_pack16_f32": (C.c_int, [P, I64, I64, I64, F64, F64, I32, P, P]),
     "tg_median_f32": (C.c_int, [P, U64, C.POINTER(C.c_float), P]),
     "tg_coastline_mask": (C.c_int, [P, I64, F64, P, C.POINTER(I64), P]),
     "tg_coastline_boxcount": (C.c_int, [P, I64, F64, P, I32, P, C.POINTER(I64), C.POINTER(I64), P]),

@@ -143,6 +143,31 @@ __global__ void rescale_kernel(float* __restrict__ x, uint64_t n, double lo, dou
         x[i] = static_cast<float>(-1.0 + 2.0 * (static_cast<double>(x[i]) - lo) / span);  // fbm.hpp:653
 }
 
+// quantize16 (io.hpp:61-65): lround((v - lo)/(hi - lo) * 65535) in fp64 on
+// the fp32 map widened exactly, written big-endian; with png_rows each row is
+// prefixed by PNG filter byte 0 (io.hpp:228-239).  lround = round half away
+// from zero; t >= 0 here so it is floor(x) + (frac >= 0.5).
+__global__ void pack16_kernel(const float* __restrict__ m, int64_t W, int64_t H, int64_t ld, double lo,
+                              double hi, int png_rows, unsigned char* __restrict__ out) {
+    const int64_t row_bytes = 2 * W + (png_rows ? 1 : 0);
+    for (int64_t y = blockIdx.x; y < H; y += gridDim.x) {
+        unsigned char* o = out + y * row_bytes;
+        if (png_rows && threadIdx.x == 0) o[0] = 0;
+        unsigned char* os = o + (png_rows ? 1 : 0);
+        for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
+            uint32_t s = 0;
+            if (hi != lo) {
+                const double t = __ddiv_rn(__dsub_rn(static_cast<double>(m[y * ld + x]), lo), __dsub_rn(hi, lo));
+                const double v = __dmul_rn(t, 65535.0);
+                const double f = floor(v);
+                s = static_cast<uint32_t>(f) + (__dsub_rn(v, f) >= 0.5 ? 1u : 0u);
+            }
+            os[2 * x] = static_cast<unsigned char>(s >> 8);
+            os[2 * x + 1] = static_cast<unsigned char>(s & 0xFF);
+        }
+    }
+}
+
 // Eight independent FFMA chains per thread: issue-bound FP32 peak.
 __global__ void ffma_kernel(float* out, int iters) {
     float a0 = threadIdx.x * 1e-7f, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
@@ -203,6 +228,19 @@ int tg_rescale_f32(float* dev_map, uint64_t n, double lo, double hi, void* strea
                                                                                  hi - lo);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return tg::set_cuda_error(e, "rescale");
+    return TG_OK;
+}
+
+int tg_pack16_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld, double lo, double hi,
+                  int32_t png_rows, uint8_t* dev_out, void* stream) {
+    if (!dev_map || !dev_out || width < 1 || height < 1 || ld < width)
+        return tg::set_error(TG_EVALIDATION, "pack16: bad arguments");
+    if (int st = tg::check_device()) return st;
+    const int blocks = static_cast<int>(height < 148 * 8 ? height : 148 * 8);
+    tg::pack16_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(dev_map, width, height, ld, lo, hi,
+                                                                             png_rows, dev_out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "pack16");
     return TG_OK;
 }
 

@@ -395,6 +395,52 @@ def variogram_dimension(sum_sq, pairs, lags) -> tuple:
     return gam, hurst, 3.0 - hurst, fit.r2
 
 
+def _pack16(dev_map, width: int, height: int, png: bool):
+    import torch
+
+    lo, hi = C.c_double(), C.c_double()
+    _check(_abi.load().tg_minmax_f32(dev_map.data_ptr(), width * height, C.byref(lo), C.byref(hi),
+                                     _stream_ptr(None)))
+    nbytes = height * (2 * width + (1 if png else 0))
+    out = torch.empty(nbytes, dtype=torch.uint8, device=dev_map.device)
+    _check(_abi.load().tg_pack16_f32(dev_map.data_ptr(), width, height, width, lo.value, hi.value,
+                                     1 if png else 0, out.data_ptr(), _stream_ptr(None)))
+    return out.cpu().numpy().tobytes(), lo.value, hi.value
+
+
+def encode_pgm16(dev_map, width: int, height: int) -> bytes:
+    """write_pgm16 (io.hpp:91-106) of a contiguous CUDA fp32 map: range and
+    quantize16 on the device, header on the host."""
+    body, lo, hi = _pack16(dev_map, width, height, False)
+    return f"P5\n# hmin={lo:.17g} hmax={hi:.17g}\n{width} {height}\n65535\n".encode() + body
+
+
+def encode_png16(dev_map, width: int, height: int) -> bytes:
+    """write_png16 (io.hpp:203-250): device-packed raw rows, zlib level 9."""
+    import struct
+    import zlib
+
+    raw, lo, hi = _pack16(dev_map, width, height, True)
+
+    def chunk(t: bytes, data: bytes) -> bytes:
+        return struct.pack(">I", len(data)) + t + data + struct.pack(">I", zlib.crc32(t + data) & 0xFFFFFFFF)
+
+    ihdr = struct.pack(">II", width, height) + bytes([16, 0, 0, 0, 0])
+    text = b"Comment\0" + f"hmin={lo:.17g} hmax={hi:.17g}".encode()
+    return (bytes([137, 80, 78, 71, 13, 10, 26, 10]) + chunk(b"IHDR", ihdr) + chunk(b"tEXt", text)
+            + chunk(b"IDAT", zlib.compress(raw, 9)) + chunk(b"IEND", b""))
+
+
+def write_pgm16(path: str, dev_map, width: int, height: int) -> None:
+    with open(path, "wb") as f:
+        f.write(encode_pgm16(dev_map, width, height))
+
+
+def write_png16(path: str, dev_map, width: int, height: int) -> None:
+    with open(path, "wb") as f:
+        f.write(encode_png16(dev_map, width, height))
+
+
 def generate3d_device(cfg: FbmConfig, origin, shape, out, stream=None) -> None:
     """3D fBm volume (new): out is a CUDA fp32 tensor [nz, ny, nx]."""
     nz, ny, nx = shape

@@ -3,12 +3,14 @@
 // terrain_b200::fbm on the B200, with the C restatement (oracle/oracle.c) as
 // the checker.  Built and run by tests/test_cpp_dropin.py.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
 
 #include "terrain_b200/analysis.hpp"
 #include "terrain_b200/fbm.hpp"
+#include "terrain_b200/io.hpp"
 
 extern "C" {
 #include "../../oracle/oracle.h"
@@ -236,6 +238,26 @@ int main() {
         const std::vector<double> ps{0.5};
         const auto rows = analysis::dimension_vs_octaves(cfg, 1, 3, ps, analysis::default_box_sizes());
         EXPECT(rows.size() == 3u && rows[2].octaves == 3, "sweep rows");
+    }
+    // PGM16 / PNG16 export of a device map (compared byte-for-byte with the
+    // reference writers by tests/test_cpp_dropin.py)
+    {
+        FbmConfig cfg;
+        cfg.seed = 5;
+        cfg.smoothstep = 5;
+        cfg.resolution = 1024;
+        cfg.base_frequency = 4;
+        cfg.octaves = 10;
+        float* d = nullptr;
+        cudaMalloc(&d, sizeof(float) * 300 * 200);
+        generate_device(cfg, {0, 0}, 300, 200, d, 300);
+        cudaDeviceSynchronize();
+        const char* dir = std::getenv("TG_OUT_DIR");
+        const std::string base = dir ? dir : "/tmp";
+        io::write_pgm16(base + "/dropin_300x200.pgm", d, 300, 200);
+        io::write_png16(base + "/dropin_300x200.png", d, 300, 200);
+        cudaFree(d);
+        EXPECT(true, "pgm/png written");
     }
     std::printf("%d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;

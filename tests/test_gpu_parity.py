@@ -463,3 +463,20 @@ def test_opensimplex_region_and_zero():
     assert torch.equal(gen(c, 32, 32, 32), gen(c, 0, 0, 64)[32:, 32:])
     c.zero_lattice = 1
     assert torch.count_nonzero(gen(c, 0, 0, 64)).item() == 0
+
+
+# ---- PGM16 / PNG16 export of device maps --------------------------
+
+@pytest.mark.skipif(not __import__("os").path.exists(__import__("os").path.join(
+    __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))),
+    "oracle", "_ref", "libtgref.so")), reason="reference build absent")
+@pytest.mark.parametrize("W,H", [(257, 257), (512, 512), (1024, 96)])
+def test_pgm_png_bytes_equal_reference_writers(W, H):
+    from oracle.pyoracle import Reference
+
+    ref = Reference()
+    c = make_cfg(method=0, smoothstep=5, seed=5, resolution=1024, base_frequency=4, octaves=10)
+    m = gen(c, 0, 0, W, H)
+    host = m.cpu().numpy().astype(np.float64)
+    assert pt.encode_pgm16(m, W, H) == ref.encode16(host, png=False)
+    assert pt.encode_png16(m, W, H) == ref.encode16(host, png=True)
