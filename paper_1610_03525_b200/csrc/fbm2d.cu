@@ -369,12 +369,9 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
             for (int cy = (warp << sh) + rs; cy < Hm; cy += rstep) {
                 const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
-                float4 v;
-                v.x = height_scaled(p);
-                v.y = height_scaled(add64(p, kIxMul));
-                v.z = height_scaled(add64(p, 2 * kIxMul));
-                v.w = height_scaled(add64(p, 3 * kIxMul));
-                *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = v;
+                float h[4];
+                height_scaled4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
+                *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
             }
             for (int i = tid; i < Hm + 1 + Wm; i += kThreads) {
                 const int cx = i <= Hm ? Wm : i - Hm - 1;
@@ -566,8 +563,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const uint64_t dY = static_cast<uint64_t>(k) * kIyMul;
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
+                float h[4];
+                height_scaled4(add64(X[0], Y), add64(X[1], Y), add64(X[2], Y), add64(X[3], Y), h);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, height_scaled(add64(X[j], Y)), acc[r][j]);
+                for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, h[j], acc[r][j]);
                 Y = add64(Y, dY);
             }
         }

@@ -86,6 +86,28 @@ __device__ __forceinline__ float height_scaled_from_pre(uint32_t lo, uint32_t hi
     return f;
 }
 
+// Four independent keys in lock step: the same 12-instruction chain per key,
+// interleaved in program order so each warp has 4-way instruction-level
+// parallelism through the 4-5 cycle IMAD/ALU latencies (a single fmix64
+// chain is fully serial).
+__device__ __forceinline__ void height_scaled4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3,
+                                              float (&out)[4]) {
+    uint32_t l[4] = {static_cast<uint32_t>(p0), static_cast<uint32_t>(p1), static_cast<uint32_t>(p2),
+                     static_cast<uint32_t>(p3)};
+    uint32_t h[4] = {static_cast<uint32_t>(p0 >> 32), static_cast<uint32_t>(p1 >> 32),
+                     static_cast<uint32_t>(p2 >> 32), static_cast<uint32_t>(p3 >> 32)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) TG_MUL64(l[i], h[i], 0xED558CCD, 0xFF51AFD7);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) TG_MUL64(l[i], h[i], 0x1A85EC53, 0xC4CEB9FE);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = height_scaled_from_pre(l[i], h[i]);
+}
+
 __device__ __forceinline__ float height_scaled(uint64_t packed) {
     uint32_t lo, hi;
     mix64_pre(packed, lo, hi);
