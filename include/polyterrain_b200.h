@@ -151,6 +151,13 @@ int tg_fbm_generate_f64_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, i
 int tg_fbm_generate_f32_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
                              float* host_out, uint64_t n_out);
 
+/* texture::render (texture.hpp:50-72) of the full R x R map: kind 0 marble,
+ * 1 wood — sin(2*pi*f*phase + gain*noise) fused into the generation store —
+ * 2 cloud (noise normalised to [-1, 1]).  Stream-ordered for marble/wood,
+ * synchronous for cloud. */
+int tg_texture_generate_f32(const tg_fbm_config* cfg, int32_t kind, double gain,
+                            double pattern_frequency, float* dev_out, void* stream);
+
 /* 3D fBm volume (new): separable zero-gradient cells
  * (method TG_METHOD_ZG_SEPARABLE only), layout [(z*ny + y)*nx + x]. */
 int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t oz,
@@ -183,6 +190,12 @@ int tg_rescale_f32(float* dev_map, uint64_t n, double lo, double hi, void* strea
  * Stream-ordered; the caller writes the header / zlib-compresses on the host. */
 int tg_pack16_f32(const float* dev_map, int64_t width, int64_t height, int64_t ld, double lo,
                   double hi, int32_t png_rows, uint8_t* dev_out, void* stream);
+
+/* Gradient-norm (hessian = 0) or Hessian-norm (1) map of a width x height
+ * device map (terrain_cli.cpp:148-182: central differences, clamped borders,
+ * fp64 arithmetic, fp32 result).  Stream-ordered. */
+int tg_norm_map_f32(const float* dev_map, int64_t width, int64_t height, int32_t hessian,
+                    float* dev_out, void* stream);
 
 /* ---- fractal analysis (analysis.hpp:213-305; variogram new) --------------- */
 

@@ -660,3 +660,27 @@ int or_variogram(const double* z, int64_t W, int64_t H, const int32_t* lags, int
     }
     return TG_OK;
 }
+
+/* gradient_norm_map / hessian_norm_map (tools/terrain_cli.cpp:148-182):
+ * central differences inside, clamped at the borders, pixel units. */
+int or_norm_map(const double* m, int64_t W, int64_t H, int hessian, double* out) {
+#define AT(xx, yy) m[(yy) * W + (xx)]
+    for (int64_t y = 0; y < H; ++y) {
+        const int64_t ym = y > 0 ? y - 1 : 0, yp = y + 1 < H ? y + 1 : H - 1;
+        for (int64_t x = 0; x < W; ++x) {
+            const int64_t xm = x > 0 ? x - 1 : 0, xp = x + 1 < W ? x + 1 : W - 1;
+            if (!hessian) {
+                const double gx = 0.5 * (AT(xp, y) - AT(xm, y));
+                const double gy = 0.5 * (AT(x, yp) - AT(x, ym));
+                out[y * W + x] = sqrt(gx * gx + gy * gy);
+            } else {
+                const double hxx = AT(xp, y) - 2.0 * AT(x, y) + AT(xm, y);
+                const double hyy = AT(x, yp) - 2.0 * AT(x, y) + AT(x, ym);
+                const double hxy = 0.25 * (AT(xp, yp) - AT(xm, yp) - AT(xp, ym) + AT(xm, ym));
+                out[y * W + x] = sqrt(hxx * hxx + 2.0 * hxy * hxy + hyy * hyy);
+            }
+        }
+    }
+#undef AT
+    return TG_OK;
+}

@@ -79,6 +79,7 @@ class Oracle:
             "or_box_count": (C.c_int, [P, I64, P, I32, P, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
             "or_linear_fit": (C.c_int, [P, P, I64, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
             "or_variogram": (C.c_int, [P, I64, I64, P, I32, P, P]),
+            "or_norm_map": (C.c_int, [P, I64, I64, C.c_int, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -179,6 +180,12 @@ class Oracle:
         st = self.lib.or_linear_fit(_ptr(x), _ptr(y), len(x), C.byref(s), C.byref(i), C.byref(r))
         return st, s.value, i.value, r.value
 
+    def norm_map(self, z: np.ndarray, hessian: bool) -> np.ndarray:
+        d = np.ascontiguousarray(z, dtype=np.float64)
+        out = np.zeros_like(d)
+        self.lib.or_norm_map(_ptr(d), d.shape[1], d.shape[0], 1 if hessian else 0, _ptr(out))
+        return out
+
     def variogram(self, z: np.ndarray, lags):
         d = np.ascontiguousarray(z, dtype=np.float64)
         lg = np.asarray(lags, dtype=np.int32)
@@ -220,6 +227,7 @@ class Reference:
             "ref_linear_fit": (C.c_int, [P, P, I32, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
             "ref_run_bench": (C.c_int, [PCFG, I32, I32, C.POINTER(F64), C.POINTER(F64), C.POINTER(F64)]),
             "ref_encode_pgm16": (I64, [P, I32, I32, P, I64]),
+            "ref_texture": (C.c_int, [PCFG, I32, F64, F64, P]),
             "ref_encode_png16": (I64, [P, I32, I32, P, I64]),
         }
         for name, (res, args) in sig.items():
@@ -314,6 +322,14 @@ class Reference:
         st = self.lib.ref_box_count_mask(_ptr(m), m.shape[0], _ptr(sz), len(sz), _ptr(counts),
                                          C.byref(d), C.byref(k), C.byref(r2))
         return st, counts, d.value, k.value, r2.value
+
+    def texture(self, cfg, kind: int, gain: float, pattern_frequency: float) -> np.ndarray:
+        R = cfg.resolution
+        out = np.zeros((R, R))
+        st = self.lib.ref_texture(C.byref(cfg), kind, gain, pattern_frequency, _ptr(out))
+        if st != 0:
+            raise ValueError(self.last_error())
+        return out
 
     def encode16(self, data: np.ndarray, png: bool) -> bytes:
         d = np.ascontiguousarray(data, dtype=np.float64)

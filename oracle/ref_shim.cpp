@@ -21,6 +21,7 @@
 #include "terrain/io.hpp"
 #include "terrain/kernels2d.hpp"
 #include "terrain/lattice.hpp"
+#include "terrain/texture.hpp"
 
 #include "../include/polyterrain_b200.h"
 
@@ -337,6 +338,21 @@ int64_t ref_encode_png16(const double* data, int32_t width, int32_t height, uint
         g_err = e.what();
         return -1;
     }
+}
+
+// texture::render (texture.hpp:50-72): full R x R map into out.
+int ref_texture(const tg_fbm_config* c, int32_t kind, double gain, double pattern_frequency, double* out) {
+    fbm::FbmConfig cfg;
+    if (!to_ref(c, cfg)) return TG_EVALIDATION;
+    return guard([&] {
+        texture::TextureSpec spec;
+        spec.kind = static_cast<texture::Kind>(kind);
+        spec.fbm = cfg;
+        spec.gain = gain;
+        spec.pattern_frequency = pattern_frequency;
+        const auto hm = texture::render(spec);
+        std::copy(hm.data.begin(), hm.data.end(), out);
+    });
 }
 
 // linear_fit (analysis.hpp:29-63).

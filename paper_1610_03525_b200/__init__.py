@@ -11,5 +11,5 @@ from .fbm import (  # noqa: F401
     default_box_sizes, ffma_peak_tflops, generate3d_device, generate_batch_device, generate_heightmap,
     generate_into, generate_into_device, generate_rect_device, generate_region, linear_fit,
     method_name, normalize_map, octave_spec, parse_method, upper_median_device, variogram_device,
-    variogram_dimension, encode_pgm16, encode_png16, write_pgm16, write_png16,
+    variogram_dimension, TextureKind, texture_device, norm_map_device, encode_pgm16, encode_png16, write_pgm16, write_png16,
 )

@@ -96,6 +96,8 @@ SIGNATURES = {
     "tg_fbm_generate_batch_f32": (C.c_int, [PCFG, P, I32, I64, I64, I64, I64, P, P]),
     "tg_fbm_generate_f64_host": (C.c_int, [PCFG, I64, I64, I64, P, U64]),
     "tg_fbm_generate_f32_host": (C.c_int, [PCFG, I64, I64, I64, P, U64]),
+    "tg_texture_generate_f32": (C.c_int, [PCFG, I32, F64, F64, P, P]),
+    "tg_norm_map_f32": (C.c_int, [P, I64, I64, I32, P, P]),
     "tg_fbm3d_generate_f32": (C.c_int, [PCFG, I64, I64, I64, I64, I64, I64, P, P]),
     "tg_lattice_hash": (C.c_int, [P, U64, U64, P, P]),
     "tg_lattice_height_f32": (C.c_int, [P, U64, P, P]),

@@ -355,6 +355,37 @@ int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_
     return tg_fbm_generate_rect_f32(cfg, ox, oy, extent, extent, dev_out, extent, stream);
 }
 
+// texture::render (texture.hpp:50-72): marble / wood fused into the fBm
+// store; cloud = the noise normalised to [-1, 1] (device min/max + rescale).
+int tg_texture_generate_f32(const tg_fbm_config* cfg, int32_t kind, double gain, double pattern_frequency,
+                            float* dev_out, void* stream) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (kind < 0 || kind > 2) return fail(TG_EVALIDATION, "texture: unknown kind");
+    if (!(pattern_frequency > 0.0) || !std::isfinite(pattern_frequency))
+        return fail(TG_EVALIDATION, "TextureSpec: pattern frequency must be positive");
+    if (!std::isfinite(gain)) return fail(TG_EVALIDATION, "TextureSpec: non-finite gain");
+    if (!dev_out) return fail(TG_EVALIDATION, "texture: null output");
+    if (cfg->resolution > TG_MAX_EXTENT) return fail(TG_EVALIDATION, "texture: resolution above the extent cap");
+    if (int st = device_ready()) return st;
+    const int64_t R = cfg->resolution;
+    tg::FbmArgs a;
+    if (int st = build_args(cfg, 0, 0, R, R, R, &a)) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (kind != 2) {  // TG texture kinds: 0 marble, 1 wood, 2 cloud
+        a.epilogue = kind == 0 ? 1 : 2;
+        a.tex_freq2pi = static_cast<float>(2.0 * 3.14159265358979323846 * pattern_frequency);
+        a.tex_gain = static_cast<float>(gain);
+    }
+    TG_CUDA(tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, dev_out, s));
+    if (kind == 2) {
+        double lo = 0, hi = 0;
+        if (int st = tg_minmax_f32(dev_out, static_cast<uint64_t>(R * R), &lo, &hi, stream)) return st;
+        if (hi > lo)
+            if (int st = tg_rescale_f32(dev_out, static_cast<uint64_t>(R * R), lo, hi, stream)) return st;
+    }
+    return TG_OK;
+}
+
 int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, int32_t n_seeds,
                               int64_t ox, int64_t oy, int64_t width, int64_t height,
                               float* dev_out, void* stream) {

@@ -738,8 +738,25 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     for (int r = 0; r < 8; ++r, row += args.ld) {
         const int64_t ly = ly0 + r;
         if (ly < 0 || ly >= args.height) continue;
-        const float v0 = acc[r][0] + racc[r], v1 = acc[r][1] + racc[r];
-        const float v2 = acc[r][2] + racc[r], v3 = acc[r][3] + racc[r];
+        float v0 = acc[r][0] + racc[r], v1 = acc[r][1] + racc[r];
+        float v2 = acc[r][2] + racc[r], v3 = acc[r][3] + racc[r];
+        if (args.epilogue) {
+            // texture::render (texture.hpp:57-68) fused into the store:
+            // sin(2 pi f phase + gain * noise), (u, v) pixel centres in [0, 1)
+            const float invR = static_cast<float>(1.0 / args.R);
+            const float vv = (static_cast<float>(ty0 + r0 + r) + 0.5f) * invR;
+            float w[4] = {v0, v1, v2, v3};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float u = (static_cast<float>(tx0 + c0 + j) + 0.5f) * invR;
+                const float phase = args.epilogue == 1 ? u : sqrtf((u - 0.5f) * (u - 0.5f) + (vv - 0.5f) * (vv - 0.5f));
+                w[j] = sinf(fmaf(args.tex_freq2pi, phase, args.tex_gain * w[j]));
+            }
+            v0 = w[0];
+            v1 = w[1];
+            v2 = w[2];
+            v3 = w[3];
+        }
         if (vec_ok) {
             *reinterpret_cast<float4*>(row) = make_float4(v0, v1, v2, v3);
         } else {

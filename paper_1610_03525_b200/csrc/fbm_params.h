@@ -90,7 +90,9 @@ struct FbmArgs {
     int32_t octaves;
     int32_t zero;            // ZeroSource
     int32_t n_maps;
-    int32_t pad;
+    int32_t epilogue;        // 0 none, 1 marble, 2 wood (texture.hpp:50-72, fused into the store)
+    float tex_freq2pi;       // 2*pi*pattern_frequency
+    float tex_gain;          // turbulence gain
     // Row LUT of the smoothstep order in use: for ppc = 2^k, entries
     // lut[2^k - 1 + r] = (x, S(x), S(x) - x, x*S(x)) with x = (r + 0.5)/ppc
     // (kernels2d.hpp:214-239 at phase 0.5), computed in fp64 and rounded.

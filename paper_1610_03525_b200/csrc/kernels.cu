@@ -168,6 +168,33 @@ __global__ void pack16_kernel(const float* __restrict__ m, int64_t W, int64_t H,
     }
 }
 
+// gradient / Hessian norm maps (terrain_cli.cpp:148-182): central
+// differences inside, clamped at the borders, in fp64 on the fp32 map widened
+// exactly, one rounding to fp32 at the end.
+__global__ void stencil_kernel(const float* __restrict__ m, int64_t W, int64_t H, int hessian,
+                               float* __restrict__ out) {
+    for (int64_t y = blockIdx.x; y < H; y += gridDim.x) {
+        const int64_t ym = y > 0 ? y - 1 : 0, yp = y + 1 < H ? y + 1 : H - 1;
+        for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
+            const int64_t xm = x > 0 ? x - 1 : 0, xp = x + 1 < W ? x + 1 : W - 1;
+            const auto at = [&](int64_t xx, int64_t yy) { return static_cast<double>(m[yy * W + xx]); };
+            double v;
+            if (!hessian) {
+                const double gx = 0.5 * (at(xp, y) - at(xm, y));
+                const double gy = 0.5 * (at(x, yp) - at(x, ym));
+                v = sqrt(gx * gx + gy * gy);
+            } else {
+                const double c = at(x, y);
+                const double hxx = at(xp, y) - 2.0 * c + at(xm, y);
+                const double hyy = at(x, yp) - 2.0 * c + at(x, ym);
+                const double hxy = 0.25 * (at(xp, yp) - at(xm, yp) - at(xp, ym) + at(xm, ym));
+                v = sqrt(hxx * hxx + 2.0 * hxy * hxy + hyy * hyy);
+            }
+            out[y * W + x] = static_cast<float>(v);
+        }
+    }
+}
+
 // Eight independent FFMA chains per thread: issue-bound FP32 peak.
 __global__ void ffma_kernel(float* out, int iters) {
     float a0 = threadIdx.x * 1e-7f, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
@@ -241,6 +268,19 @@ int tg_pack16_f32(const float* dev_map, int64_t width, int64_t height, int64_t l
                                                                              png_rows, dev_out);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return tg::set_cuda_error(e, "pack16");
+    return TG_OK;
+}
+
+int tg_norm_map_f32(const float* dev_map, int64_t width, int64_t height, int32_t hessian, float* dev_out,
+                    void* stream) {
+    if (!dev_map || !dev_out || width < 1 || height < 1 || dev_map == dev_out)
+        return tg::set_error(TG_EVALIDATION, "norm map: bad arguments");
+    if (int st = tg::check_device()) return st;
+    const int blocks = static_cast<int>(height < 148 * 8 ? height : 148 * 8);
+    tg::stencil_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(dev_map, width, height,
+                                                                              hessian ? 1 : 0, dev_out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return tg::set_cuda_error(e, "norm map");
     return TG_OK;
 }
 

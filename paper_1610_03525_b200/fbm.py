@@ -441,6 +441,28 @@ def write_png16(path: str, dev_map, width: int, height: int) -> None:
         f.write(encode_png16(dev_map, width, height))
 
 
+class TextureKind(enum.IntEnum):
+    """terrain::texture::Kind (texture.hpp:19)."""
+
+    marble = 0
+    wood = 1
+    cloud = 2
+
+
+def texture_device(cfg: FbmConfig, kind: TextureKind, out, gain: float = 1.0, pattern_frequency: float = 4.0,
+                   stream=None) -> None:
+    """texture::render (texture.hpp:50-72) of the full map into a CUDA fp32
+    tensor; marble/wood are fused into the generation store."""
+    _check(_abi.load().tg_texture_generate_f32(C.byref(cfg.to_c()), int(kind), float(gain),
+                                               float(pattern_frequency), out.data_ptr(), _stream_ptr(stream)))
+
+
+def norm_map_device(dev_map, width: int, height: int, out, hessian: bool = False, stream=None) -> None:
+    """gradient_norm_map / hessian_norm_map (terrain_cli.cpp:148-182) on the device."""
+    _check(_abi.load().tg_norm_map_f32(dev_map.data_ptr(), width, height, 1 if hessian else 0, out.data_ptr(),
+                                       _stream_ptr(stream)))
+
+
 def generate3d_device(cfg: FbmConfig, origin, shape, out, stream=None) -> None:
     """3D fBm volume (new): out is a CUDA fp32 tensor [nz, ny, nx]."""
     nz, ny, nx = shape

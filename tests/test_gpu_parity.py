@@ -480,3 +480,34 @@ def test_pgm_png_bytes_equal_reference_writers(W, H):
     host = m.cpu().numpy().astype(np.float64)
     assert pt.encode_pgm16(m, W, H) == ref.encode16(host, png=False)
     assert pt.encode_png16(m, W, H) == ref.encode16(host, png=True)
+
+
+# ---- texture epilogue and gradient / Hessian norm maps -------
+
+@pytest.mark.skipif(not __import__("os").path.exists(__import__("os").path.join(
+    __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))),
+    "oracle", "_ref", "libtgref.so")), reason="reference build absent")
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("method", [0, 3])
+def test_texture_matches_reference_render(kind, method):
+    from oracle.pyoracle import Reference
+
+    c = make_cfg(method=method, seed=31, resolution=512, base_frequency=4, octaves=6)
+    out = torch.empty((512, 512), dtype=torch.float32, device="cuda")
+    assert _abi.load().tg_texture_generate_f32(C.byref(c), kind, 2.5, 4.0, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    ref = Reference().texture(c, kind, 2.5, 4.0)
+    err = float(np.max(np.abs(out.cpu().numpy().astype(np.float64) - ref)))
+    assert err <= 1e-5, err  # values in [-1, 1]
+
+
+def test_norm_maps_match_restated_cli_stencils(oracle):
+    c = make_cfg(method=0, smoothstep=5, seed=8, resolution=512, base_frequency=4, octaves=8)
+    m = gen(c, 0, 0, 320, 200)
+    host = m.cpu().numpy().astype(np.float64)
+    for hess in (False, True):
+        out = torch.empty_like(m)
+        pt.norm_map_device(m, 320, 200, out, hessian=hess)
+        torch.cuda.synchronize()
+        ref = oracle.norm_map(host, hess).astype(np.float32)
+        assert np.array_equal(out.cpu().numpy(), ref)
