@@ -228,12 +228,12 @@ constexpr size_t smem_bytes() {
 // gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners
 // (q = amp/4, folded with the grid's 2^-63 height scale).
 template <class Fetch>
-__device__ __forceinline__ void ppc1_block(float (&acc)[8][4], float q, Fetch fetch) {
+__device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch fetch) {
     float h[5];
     fetch(0, h);
     float hs[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < kRPT; ++r) {
         fetch(r + 1, h);
         const float ns[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
 #pragma unroll
@@ -247,7 +247,7 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[8][4], float q, Fetch fe
 // zero-gradient cell rows r_begin.. of one cell: c0 = h00 + sy*dy goes into
 // the per-row accumulator (common to the 4 columns), the rest per pixel.
 template <int KIND, int NR>
-__device__ __forceinline__ void zg_rows(float (&acc)[8][4], float (&racc)[8], int r_begin,
+__device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRPT], int r_begin,
                                         const float4* __restrict__ Ly, const float (&x)[4],
                                         const float (&sx)[4], float h00, float h10, float h01,
                                         float h11) {
@@ -290,7 +290,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     const int64_t ty0 = args.tile_y0 + static_cast<int64_t>(blockIdx.y) * kTH;
     const uint64_t seed_key = args.seed_key[blockIdx.z];
     const int c0 = lane * 4;
-    const int r0 = warp * 8;
+    const int r0 = warp * kRPT;
 
     // Grid contents: zero-gradient grids hold raw height_scaled() values (the
     // octave amplitude is folded in at evaluation); Perlin/generic grids hold
@@ -408,10 +408,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     __syncthreads();
 
     // ---- evaluation of the thread's 4 x 8 pixels (no barriers) --------------
-    float acc[8][4];
-    float racc[8];  // per-row terms common to the 4 columns (zg block modes)
+    float acc[kRPT][4];
+    float racc[kRPT];  // per-row terms common to the 4 columns (zg block modes)
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < kRPT; ++r) {
         racc[r] = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
@@ -434,7 +434,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 x[j] = e.x;
                 sx[j] = e.y;
             }
-            zg_rows<KIND, 8>(acc, racc, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
+            zg_rows<KIND, kRPT>(acc, racc, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
                              amp * g[od.pitch + 1]);
         }
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
@@ -453,9 +453,11 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             }
             const float a0 = amp * g[0], a1 = amp * g[1];
             const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
-            const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
             zg_rows<KIND, 4>(acc, racc, 0, L, x, sx, a0, a1, b0, b1);
-            zg_rows<KIND, 4>(acc, racc, 4, L, x, sx, b0, b1, e0, e1);
+            if constexpr (kRPT == 8) {
+                const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
+                zg_rows<KIND, 4>(acc, racc, 4, L, x, sx, b0, b1, e0, e1);
+            }
         }
     }
 
@@ -473,7 +475,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 #pragma unroll
             for (int c = 0; c < CH; ++c) t[u][c] = sc * g[c * kGridCap + u];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kRPT / 2; ++k) {
             const float* gn = g + (k + 1) * pitch;
             float b[3][CH];
 #pragma unroll
@@ -534,7 +536,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             float at[5], bt[5];
             load(0, at, bt);
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRPT; ++r) {
                 float ab[5], bb[5];
                 load(r + 1, ab, bb);
 #pragma unroll
@@ -562,7 +564,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             uint64_t Y = seed_key + od.oct_key + static_cast<uint64_t>((ty0 + r0) * k + half) * kIyMul;
             const uint64_t dY = static_cast<uint64_t>(k) * kIyMul;
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRPT; ++r) {
                 float h[4];
                 height_scaled4(add64(X[0], Y), add64(X[1], Y), add64(X[2], Y), add64(X[3], Y), h);
 #pragma unroll
@@ -599,7 +601,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             Cell<KIND> cell;
             int last = -1;
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRPT; ++r) {
                 const int yr = yo + r;
                 const int ry = yr >> sh;
                 const float4 f = L[yr & mask];
@@ -640,7 +642,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             int last_key = -1;
             Cell<KIND> cell;
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRPT; ++r) {
                 const float4 f = tb.rowF[r0 + r];
                 const float y = f.x, sy = f.y;
                 const int ry = __float_as_int(f.w) * pitch;
@@ -704,7 +706,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 xs[j] = x[j] * sx[j];
             }
 #pragma unroll 1
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRPT; ++r) {
                 int64_t iy;
                 float y;
                 axis_coord(od, args.R, ty0 + r0 + r, &iy, &y);
@@ -720,7 +722,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                     cj.make(k00, k10, k01, k11);
                     const float v = Cell<KIND>::eval(cj.row(y, sy), x[j], sx[j], xs[j]);
 #pragma unroll
-                    for (int rr = 0; rr < 8; ++rr)
+                    for (int rr = 0; rr < kRPT; ++rr)
                         if (rr == r) acc[rr][j] += v;
                 }
             }
@@ -735,7 +737,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                         ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && lx0 >= 0 &&
                         lx0 + 4 <= args.width;
 #pragma unroll
-    for (int r = 0; r < 8; ++r, row += args.ld) {
+    for (int r = 0; r < kRPT; ++r, row += args.ld) {
         const int64_t ly = ly0 + r;
         if (ly < 0 || ly >= args.height) continue;
         float v0 = acc[r][0] + racc[r], v1 = acc[r][1] + racc[r];

@@ -27,9 +27,13 @@ constexpr int kMaxOctaves = 32;
 constexpr int kMaxBatch = 64;
 
 // 2D tile geometry and per-CTA shared-memory budget (fbm2d.cu).
+#ifndef TG_RPT
+#define TG_RPT 8                   // pixel rows per thread (4 or 8)
+#endif
+constexpr int kRPT = TG_RPT;
 constexpr int kTileW = 128;        // 32 lanes x 4 columns
-constexpr int kTileH = 64;         // 8 warps x 8 rows
-constexpr int kGridCap = 12288;    // lattice-corner floats per channel per CTA
+constexpr int kTileH = 8 * kRPT;   // 8 warps x kRPT rows
+constexpr int kGridCap = kRPT == 8 ? 12288 : 6656;  // lattice-corner floats per channel per CTA
 constexpr int kTabSlots = 4;       // per-CTA sampling tables (general octaves)
 constexpr int kLutLog2Max = 13;    // device row LUT covers ppc = 1 .. 8192
 
