@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libpolyterrain_b200.so")
-SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu"]
+SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu",
+           "hostpipe.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -41,7 +42,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     os.makedirs(LIB_DIR, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(LIB_DIR, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
@@ -54,7 +55,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         objs.append(obj)
     os.makedirs(os.path.dirname(target), exist_ok=True)
     tmp = target + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread"]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"link failed:\n{out.stderr}")

@@ -13,7 +13,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <mutex>
 #include <string>
+#include <vector>
+
+#include "hostpipe.h"
 
 #include "../../include/polyterrain_b200.h"
 #include "fbm_params.h"
@@ -410,6 +415,104 @@ int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, i
 // std::span<double>) (fbm.hpp:630-634).  Device work is fp32; the result is
 // produced in row bands so the next band's generation overlaps the previous
 // band's device->host copy.
+// Host-buffer generation (the drop-in generate_into(span<double>),
+// fbm.hpp:630-634).  Bands of whole tile rows are generated on two streams
+// and copied over PCIe as fp32 into a ring of pinned staging slots; the host
+// pool widens (exact) / copies each landed band into the caller's buffer while
+// later bands are in flight, so the bus carries 4 B/sample, not 8.  A pinned
+// fp32 destination takes the copy directly.  Staging is cached per device.
+namespace {
+
+constexpr int kSlots = 4;
+constexpr size_t kBandElems = size_t(1) << 20;  // 4 MiB of fp32 per band
+
+struct HostStage {
+    int dev = -1;
+    size_t cap = 0;  // elements per band slot
+    cudaStream_t st[2] = {nullptr, nullptr};
+    float* dbuf[2] = {nullptr, nullptr};
+    double* dwide[2] = {nullptr, nullptr};  // device-widened bands (pinned f64 destinations)
+    float* pin[kSlots] = {};
+    cudaEvent_t ev[kSlots] = {};
+};
+
+std::mutex g_stage_m;
+std::vector<HostStage*> g_stage_free;
+
+void stage_free_buffers(HostStage* s) {
+    for (auto& d : s->dbuf) if (d) cudaFree(d), d = nullptr;
+    for (auto& d : s->dwide) if (d) cudaFree(d), d = nullptr;
+    for (auto& p : s->pin) if (p) cudaFreeHost(p), p = nullptr;
+    s->cap = 0;
+}
+
+HostStage* stage_acquire(int dev, size_t cap) {
+    HostStage* s = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_stage_m);
+        for (size_t i = 0; i < g_stage_free.size(); ++i)
+            if (g_stage_free[i]->dev == dev) {
+                s = g_stage_free[i];
+                g_stage_free.erase(g_stage_free.begin() + i);
+                break;
+            }
+    }
+    if (!s) {
+        s = new HostStage;
+        s->dev = dev;
+        for (auto& st : s->st)
+            if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) st = nullptr;
+        for (auto& e : s->ev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr;
+        if (!s->st[0] || !s->st[1] || !s->ev[kSlots - 1]) {
+            cudaGetLastError();
+            return nullptr;  // leaks the half-built stage; only on a broken device
+        }
+    }
+    if (s->cap < cap) {
+        stage_free_buffers(s);
+        bool ok = true;
+        for (auto& d : s->dbuf) ok = ok && cudaMalloc(reinterpret_cast<void**>(&d), cap * sizeof(float)) == cudaSuccess;
+        for (auto& d : s->dwide) ok = ok && cudaMalloc(reinterpret_cast<void**>(&d), cap * sizeof(double)) == cudaSuccess;
+        for (auto& p : s->pin) ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&p), cap * sizeof(float), cudaHostAllocDefault) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            stage_free_buffers(s);
+            std::lock_guard<std::mutex> lk(g_stage_m);
+            g_stage_free.push_back(s);
+            return nullptr;
+        }
+        s->cap = cap;
+    }
+    return s;
+}
+
+void stage_release(HostStage* s) {
+    std::lock_guard<std::mutex> lk(g_stage_m);
+    g_stage_free.push_back(s);
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+bool env_flag(const char* name, bool dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) != 0 : dflt;
+}
+
+double env_double(const char* name, double dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atof(e) : dflt;
+}
+
+}  // namespace
+
 static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
                          void* host_out, uint64_t n_out, bool f64) {
     if (int st = validate_cfg(cfg)) return st;
@@ -420,55 +523,82 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     if (!host_out) return fail(TG_EVALIDATION, "generate: null output");
     if (int st = validate_window(cfg, ox, oy, extent, extent)) return st;
     if (int st = device_ready()) return st;
+    int dev = 0;
+    TG_CUDA(cudaGetDevice(&dev));
 
     const int64_t th = tg::fbm2d_tile_h();
-    // Bands of whole tile rows, ~8 MiB of fp32 each.
-    int64_t band = std::max<int64_t>(th, (static_cast<int64_t>(2) << 20) / extent / th * th);
+    int64_t band = std::max<int64_t>(th, static_cast<int64_t>(kBandElems) / extent / th * th);
     band = std::min<int64_t>(band, extent);
-    const size_t elem = f64 ? sizeof(double) : sizeof(float);
-    cudaStream_t st[2];
-    TG_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
-    TG_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
-    float* dev32[2] = {nullptr, nullptr};
-    double* dev64[2] = {nullptr, nullptr};
-    const size_t band_elems = static_cast<size_t>(band) * static_cast<size_t>(extent);
+    const int64_t nb = (extent + band - 1) / band;
+    const bool pinned = is_pinned(host_out);
+    const bool direct32 = !f64 && pinned;  // fp32 into pinned: one DMA per band
+    // Pinned f64 destination: bands are widened on the device and DMA'd as f64
+    // straight into the caller's buffer (8 B/sample on the bus, no host work).
+    // TG_HOST_WIDEN_FRAC moves a fraction of them to the fp32 + host-widen
+    // route; measured on the B200 host (tools/time_e2e.py) that only trades
+    // PCIe for host memory bandwidth (2.27-2.5 ms vs 2.53 ms at 4096^2, with
+    // large run-to-run spread), so the default is 0.  Pageable destinations
+    // always take the host route (a pageable DMA is driver-staged anyway).
+    double frac = f64 ? (pinned ? env_double("TG_HOST_WIDEN_FRAC", 0.0) : 1.0) : 1.0;
+    frac = std::min(1.0, std::max(0.0, frac));
+    auto host_widened = [&](int64_t i) {
+        return std::floor(static_cast<double>(i + 1) * frac) > std::floor(static_cast<double>(i) * frac);
+    };
+    const bool nt = env_flag("TG_HOST_STREAM_STORES", true);
+    HostStage* s = stage_acquire(dev, static_cast<size_t>(band) * static_cast<size_t>(extent));
+    if (!s) return fail(TG_EDEVICE, "generate: staging allocation failed");
+
     int rc = TG_OK;
-    for (int i = 0; i < 2 && rc == TG_OK; ++i) {
-        if (cudaMallocAsync(reinterpret_cast<void**>(&dev32[i]), band_elems * sizeof(float), st[i]) != cudaSuccess)
-            rc = fail(TG_EDEVICE, "generate: device allocation failed");
-        if (f64 && rc == TG_OK &&
-            cudaMallocAsync(reinterpret_cast<void**>(&dev64[i]), band_elems * sizeof(double), st[i]) != cudaSuccess)
-            rc = fail(TG_EDEVICE, "generate: device allocation failed");
-    }
-    if (rc == TG_OK) {
-        tg::FbmArgs a;
-        int bi = 0;
-        for (int64_t y0 = 0; y0 < extent && rc == TG_OK; y0 += band, bi ^= 1) {
-            const int64_t h = std::min<int64_t>(band, extent - y0);
-            if (build_args(cfg, ox, oy + y0, extent, h, extent, &a) != TG_OK) {
-                rc = TG_EDEVICE;
-                break;
-            }
-            cudaError_t e = tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, dev32[bi], st[bi]);
-            const void* src = dev32[bi];
-            if (e == cudaSuccess && f64) {
-                e = tg::widen_launch(dev32[bi], dev64[bi], static_cast<uint64_t>(h * extent), st[bi]);
-                src = dev64[bi];
-            }
-            char* dst = static_cast<char*>(host_out) + static_cast<size_t>(y0) * extent * elem;
-            if (e == cudaSuccess)
-                e = cudaMemcpyAsync(dst, src, static_cast<size_t>(h) * extent * elem,
-                                    cudaMemcpyDeviceToHost, st[bi]);
-            if (e != cudaSuccess) rc = cuda_fail(e, "generate_host");
+    auto drain = [&](int64_t j) {
+        const int slot = static_cast<int>(j % kSlots);
+        if (cudaError_t e = cudaEventSynchronize(s->ev[slot])) {
+            if (rc == TG_OK) rc = cuda_fail(e, "generate_host");
+            return;
         }
+        if (direct32 || rc != TG_OK || (f64 && !host_widened(j))) return;
+        const int64_t y0 = j * band, h = std::min<int64_t>(band, extent - y0);
+        const size_t n = static_cast<size_t>(h) * static_cast<size_t>(extent);
+        const size_t off = static_cast<size_t>(y0) * static_cast<size_t>(extent);
+        if (f64) tg::host::widen(s->pin[slot], static_cast<double*>(host_out) + off, n, nt);
+        else tg::host::copy(s->pin[slot], static_cast<float*>(host_out) + off, n, nt);
+    };
+    tg::FbmArgs a;
+    int64_t issued = 0;
+    for (int64_t i = 0; i < nb && rc == TG_OK; ++i) {
+        const int64_t y0 = i * band, h = std::min<int64_t>(band, extent - y0);
+        const int b = static_cast<int>(i & 1), slot = static_cast<int>(i % kSlots);
+        if (build_args(cfg, ox, oy + y0, extent, h, extent, &a) != TG_OK) {
+            rc = TG_EDEVICE;
+            break;
+        }
+        const size_t n = static_cast<size_t>(h) * static_cast<size_t>(extent);
+        const size_t off = static_cast<size_t>(y0) * static_cast<size_t>(extent);
+        cudaError_t e = tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a, s->dbuf[b], s->st[b]);
+        if (e == cudaSuccess) {
+            if (f64 && !host_widened(i)) {
+                e = tg::widen_launch(s->dbuf[b], s->dwide[b], n, s->st[b]);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(static_cast<double*>(host_out) + off, s->dwide[b], n * sizeof(double),
+                                        cudaMemcpyDeviceToHost, s->st[b]);
+            } else {
+                void* dst = direct32 ? static_cast<void*>(static_cast<float*>(host_out) + off) : s->pin[slot];
+                e = cudaMemcpyAsync(dst, s->dbuf[b], n * sizeof(float), cudaMemcpyDeviceToHost, s->st[b]);
+            }
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(s->ev[slot], s->st[b]);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "generate_host");
+            break;
+        }
+        issued = i + 1;
+        if (i >= kSlots - 1) drain(i - (kSlots - 1));
     }
-    for (int i = 0; i < 2; ++i) {
-        if (dev32[i]) cudaFreeAsync(dev32[i], st[i]);
-        if (dev64[i]) cudaFreeAsync(dev64[i], st[i]);
-        cudaError_t e = cudaStreamSynchronize(st[i]);
+    for (int64_t j = std::max<int64_t>(0, issued - (kSlots - 1)); j < issued; ++j) drain(j);
+    for (auto st : s->st) {
+        cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess && rc == TG_OK) rc = cuda_fail(e, "generate_host sync");
-        cudaStreamDestroy(st[i]);
     }
+    stage_release(s);
     return rc;
 }
 

@@ -1,0 +1,168 @@
+// hostpipe.cpp — persistent host worker pool + fp32->fp64 widening for the
+// host-buffer entry points (tg_fbm_generate_f64_host / _f32_host).
+//
+// The reference's generate_into writes a caller-owned span<double>
+// (fbm.hpp:541-628).  Moving doubles over PCIe doubles the bus bytes; the
+// device computes fp32 anyway, so the path ships fp32 bands (4 B/sample) into
+// pinned staging and the host widens them (exact) into the caller's buffer,
+// overlapped with the next bands' generation and copies.
+#include "hostpipe.h"
+
+#include <emmintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
+
+namespace tg {
+namespace host {
+namespace {
+
+class Pool {
+   public:
+    explicit Pool(int n) : n_(n) {
+        for (int i = 1; i < n_; ++i) std::thread([this] { loop(); }).detach();  // process lifetime
+    }
+    int size() const { return n_; }
+
+    void run(int n, const std::function<void(int)>& f) {
+        std::lock_guard<std::mutex> submit(submit_);
+        if (n_ <= 1 || n <= 1) {
+            for (int i = 0; i < n; ++i) f(i);
+            return;
+        }
+        auto job = std::make_shared<Job>();
+        job->fn = &f;
+        job->total = n;
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            job_ = job;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work(*job);
+        std::unique_lock<std::mutex> lk(m_);
+        done_cv_.wait(lk, [&] { return job->done.load() == n; });
+        job_.reset();
+    }
+
+   private:
+    // One submission; a worker that wakes late holds the old job, whose index
+    // counter is exhausted, so it can never run a stale function.
+    struct Job {
+        const std::function<void(int)>* fn = nullptr;
+        int total = 0;
+        std::atomic<int> next{0}, done{0};
+    };
+
+    void work(Job& j) {
+        int i, mine = 0;
+        while ((i = j.next.fetch_add(1)) < j.total) {
+            (*j.fn)(i);
+            ++mine;
+        }
+        if (mine && j.done.fetch_add(mine) + mine == j.total) {
+            std::lock_guard<std::mutex> lk(m_);
+            done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::shared_ptr<Job> j;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                j = job_;
+            }
+            if (j) work(*j);
+        }
+    }
+
+    int n_;
+    std::mutex submit_, m_;
+    std::condition_variable cv_, done_cv_;
+    std::shared_ptr<Job> job_;
+    uint64_t gen_ = 0;
+};
+
+Pool& pool() {
+    static Pool* p = [] {
+        int n = static_cast<int>(std::thread::hardware_concurrency());
+        n = std::min(std::max(n, 1), 8);
+        if (const char* e = std::getenv("TG_HOST_THREADS")) n = std::max(1, std::atoi(e));
+        return new Pool(n);
+    }();
+    return *p;
+}
+
+void widen_serial(const float* s, double* d, size_t n, bool stream) {
+    size_t i = 0;
+    if (stream) {
+        for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = s[i];
+        for (; i + 8 <= n; i += 8) {
+            const __m128 a = _mm_loadu_ps(s + i), b = _mm_loadu_ps(s + i + 4);
+            _mm_stream_pd(d + i, _mm_cvtps_pd(a));
+            _mm_stream_pd(d + i + 2, _mm_cvtps_pd(_mm_movehl_ps(a, a)));
+            _mm_stream_pd(d + i + 4, _mm_cvtps_pd(b));
+            _mm_stream_pd(d + i + 6, _mm_cvtps_pd(_mm_movehl_ps(b, b)));
+        }
+    }
+    for (; i < n; ++i) d[i] = s[i];
+    if (stream) _mm_sfence();
+}
+
+void copy_serial(const float* s, float* d, size_t n, bool stream) {
+    size_t i = 0;
+    if (stream) {
+        for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = s[i];
+        for (; i + 8 <= n; i += 8) {
+            _mm_stream_ps(d + i, _mm_loadu_ps(s + i));
+            _mm_stream_ps(d + i + 4, _mm_loadu_ps(s + i + 4));
+        }
+        for (; i < n; ++i) d[i] = s[i];
+        _mm_sfence();
+        return;
+    }
+    std::memcpy(d, s, n * sizeof(float));
+}
+
+template <class F>
+void split(size_t n, F&& f) {
+    const int t = pool().size();
+    // >= 64 KiB of input per piece, pieces on 64-element boundaries
+    const size_t min_piece = 16384;
+    int pieces = static_cast<int>(std::min<size_t>(static_cast<size_t>(t), (n + min_piece - 1) / min_piece));
+    pieces = std::max(pieces, 1);
+    size_t per = (n + pieces - 1) / pieces;
+    per = (per + 63) / 64 * 64;
+    pool().run(pieces, [&](int k) {
+        const size_t b = static_cast<size_t>(k) * per;
+        if (b >= n) return;
+        f(b, std::min(per, n - b));
+    });
+}
+
+}  // namespace
+
+int threads() { return pool().size(); }
+
+void parallel_for(int n, const std::function<void(int)>& f) { pool().run(n, f); }
+
+void widen(const float* src, double* dst, size_t n, bool stream) {
+    split(n, [&](size_t b, size_t m) { widen_serial(src + b, dst + b, m, stream); });
+}
+
+void copy(const float* src, float* dst, size_t n, bool stream) {
+    split(n, [&](size_t b, size_t m) { copy_serial(src + b, dst + b, m, stream); });
+}
+
+}  // namespace host
+}  // namespace tg

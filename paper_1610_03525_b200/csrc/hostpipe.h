@@ -1,0 +1,26 @@
+// hostpipe.h — host side of the drop-in generate_into(span<double>) path
+// (fbm.hpp:630-634): a persistent worker pool that widens/copies fp32 bands
+// from pinned staging into the caller's buffer while later bands are still
+// being generated and copied over PCIe.
+#pragma once
+#include <cstddef>
+#include <functional>
+
+namespace tg {
+namespace host {
+
+// Number of host threads the pool uses (TG_HOST_THREADS, default
+// min(hardware_concurrency, 8): widening is host-memory-bound well before that); 1 means the caller's thread alone.
+int threads();
+
+// Runs f(i) for i in [0, n) on the pool and the calling thread; returns when
+// all are done.  Calls from different threads are serialised.
+void parallel_for(int n, const std::function<void(int)>& f);
+
+// dst[i] = (double)src[i] / dst[i] = src[i], parallel over the pool;
+// streaming stores when `stream` (no read-for-ownership of dst).
+void widen(const float* src, double* dst, size_t n, bool stream);
+void copy(const float* src, float* dst, size_t n, bool stream);
+
+}  // namespace host
+}  // namespace tg

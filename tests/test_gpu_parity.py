@@ -235,6 +235,25 @@ def test_host_drop_in_matches_device():
     assert np.array_equal(f32.astype(np.float64), dev)
 
 
+@pytest.mark.parametrize("frac", ["0", "0.5", "1"])
+def test_host_pipeline_bands_pinned_pageable(frac, monkeypatch):
+    """Banded host path: 10 ragged bands through the 4-slot staging ring, f64
+    (device- and host-widened mixes) and f32 destinations, pinned, pageable
+    and misaligned (streaming-store head) buffers."""
+    monkeypatch.setenv("TG_HOST_WIDEN_FRAC", frac)
+    cfg = pt.FbmConfig(seed=5, resolution=4096, base_frequency=8, octaves=12, smoothstep=5)
+    E = 3000
+    dev = gen(cfg.to_c(), 0, 0, E).cpu()
+    for dt in (torch.float64, torch.float32):
+        want = dev.to(dt)
+        for pinned in (True, False):
+            t = torch.full((E * E + 1,), 7.0, dtype=dt, pin_memory=pinned)
+            for off in (0, 1):
+                view = t[off:off + E * E]
+                pt.generate_into(cfg, (0, 0), E, view.numpy())
+                assert torch.equal(view.view(E, E), want), (dt, pinned, off)
+
+
 def test_validation_errors_on_device_path():
     cfg = pt.FbmConfig(resolution=64)
     with pytest.raises(pt.ValidationError):
