@@ -8,6 +8,7 @@
 // exact, so they equal the reference run on the same fp32 map.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -35,13 +36,26 @@ struct SelectState {
 
 constexpr int kBins = 2048;
 
-// Per-block shared-memory histograms written to partials[block][bin] (no
-// global atomics), summed by hist_reduce: 2048 bins x a few hundred blocks of
-// global atomics on 2048 addresses would serialise in L2.
-constexpr int kHistBlocks = 296;
+constexpr int kHistBlocks = 148 * 4;  // 4 x 512 threads per SM
+
+// Keys outside the current prefix take no part.  Plain shared atomics: the
+// first digit (sign, exponent, 2 mantissa bits) spreads heights over a few
+// dozen bins, so same-address replays within a warp stay cheap (a match.any
+// merge measured 3x slower per element).
+__device__ __forceinline__ void hist_add(unsigned int* sh, uint32_t key, uint32_t prefix, uint32_t mask,
+                                         int shift, uint32_t dmask) {
+    if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & dmask], 1u);
+}
+
+// Shared-memory histogram flushed into the global one (non-zero bins only).
+__device__ __forceinline__ void hist_flush(const unsigned int* sh, unsigned long long* hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(sh[i]));
+}
 
 __global__ void radix_hist(const float* __restrict__ x, uint64_t n, const SelectState* st,
-                           int shift, int bits, unsigned int* __restrict__ partials) {
+                           int shift, int bits, unsigned long long* __restrict__ hist) {
     __shared__ unsigned int sh[kBins];
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -50,61 +64,82 @@ __global__ void radix_hist(const float* __restrict__ x, uint64_t n, const Select
     const uint64_t n4 = (reinterpret_cast<uintptr_t>(x) & 15) == 0 ? n / 4 : 0;
     const float4* x4 = reinterpret_cast<const float4*>(x);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    for (; i + stride < n4; i += 2 * stride) {  // two independent 16-byte loads in flight
+        const float4 v = x4[i], u = x4[i + stride];
+        hist_add(sh, fkey(v.x), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(v.y), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(v.z), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(v.w), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(u.x), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(u.y), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(u.z), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(u.w), prefix, mask, shift, dmask);
+    }
+    for (; i < n4; i += stride) {
         const float4 v = x4[i];
-        const uint32_t k[4] = {fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w)};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if ((k[u] & mask) == prefix) atomicAdd(&sh[(k[u] >> shift) & dmask], 1u);
+        hist_add(sh, fkey(v.x), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(v.y), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(v.z), prefix, mask, shift, dmask);
+        hist_add(sh, fkey(v.w), prefix, mask, shift, dmask);
     }
-    for (uint64_t i = n4 * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-        const uint32_t key = fkey(x[i]);
-        if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & dmask], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) partials[blockIdx.x * kBins + i] = sh[i];
-}
-
-__global__ void hist_reduce(const unsigned int* __restrict__ partials, int blocks,
-                            unsigned long long* __restrict__ hist) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= kBins) return;
-    unsigned long long s = 0;
-    for (int k = 0; k < blocks; ++k) s += partials[k * kBins + b];
-    hist[b] = s;
+    for (uint64_t i = n4 * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+        hist_add(sh, fkey(x[i]), prefix, mask, shift, dmask);
+    hist_flush(sh, hist);
 }
 
 // Strided-window form (row bands with halos): blocks stride over rows.
 __global__ void radix_hist2d(const float* __restrict__ x, int64_t width, int64_t rows, int64_t ld,
                              const SelectState* st, int shift, int bits,
-                             unsigned int* __restrict__ partials) {
+                             unsigned long long* __restrict__ hist) {
     __shared__ unsigned int sh[kBins];
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const uint32_t prefix = st->prefix, mask = st->mask;
     const uint32_t dmask = (1u << bits) - 1u;
     for (int64_t y = blockIdx.x; y < rows; y += gridDim.x)
-        for (int64_t i = threadIdx.x; i < width; i += blockDim.x) {
-            const uint32_t key = fkey(x[y * ld + i]);
-            if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & dmask], 1u);
-        }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) partials[blockIdx.x * kBins + i] = sh[i];
+        for (int64_t i = threadIdx.x; i < width; i += blockDim.x)
+            hist_add(sh, fkey(x[y * ld + i]), prefix, mask, shift, dmask);
+    hist_flush(sh, hist);
 }
 
-__global__ void radix_pick(SelectState* st, unsigned long long* hist, int shift, int bits) {
-    if (threadIdx.x != 0) return;
-    const int nb = 1 << bits;
-    uint64_t k = st->k, acc = 0;
-    int b = 0;
-    for (; b < nb; ++b) {
-        if (acc + hist[b] > k) break;
-        acc += hist[b];
+// Picks the digit whose cumulative count crosses the remaining rank k
+// (one block of kBins / 2 threads, two bins each), then clears the histogram
+// for the next pass.
+__global__ void __launch_bounds__(kBins / 2) radix_pick(SelectState* st, unsigned long long* hist, int shift, int bits) {
+    __shared__ unsigned long long wsum[32];
+    const int nb = 1 << bits, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned long long h0 = 2 * t < nb ? hist[2 * t] : 0, h1 = 2 * t + 1 < nb ? hist[2 * t + 1] : 0;
+    unsigned long long inc = h0 + h1;  // inclusive scan over threads
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
     }
-    st->k = k - acc;
-    st->prefix |= static_cast<uint32_t>(b) << shift;
-    st->mask |= static_cast<uint32_t>(nb - 1) << shift;
-    for (int i = 0; i < nb; ++i) hist[i] = 0;
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += v;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    const unsigned long long before = inc - h0 - h1 + (warp ? wsum[warp - 1] : 0);
+    const uint64_t k = st->k;
+    int b = -1;
+    unsigned long long acc = 0;
+    if (before <= k && k < before + h0) b = 2 * t, acc = before;
+    else if (before + h0 <= k && k < before + h0 + h1) b = 2 * t + 1, acc = before + h0;
+    __syncthreads();  // every thread has read st->k
+    if (b >= 0) {
+        st->k = k - acc;
+        st->prefix |= static_cast<uint32_t>(b) << shift;
+        st->mask |= static_cast<uint32_t>(nb - 1) << shift;
+    }
+    if (2 * t < kBins) hist[2 * t] = 0;
+    if (2 * t + 1 < kBins) hist[2 * t + 1] = 0;
 }
 
 // ---- coastline bit mask -------------------------------------------------------
@@ -133,21 +168,30 @@ __global__ void coast_bits_kernel(const float* __restrict__ h, int64_t R, int64_
         // land bits of this row and the neighbours, one word per iteration;
         // lane i ends up owning word w0 + i.
         uint32_t Lc = 0, Lu = 0, Ld = 0;
-        for (int i = 0; i < 32; ++i) {
-            const int64_t w = w0 + i;
-            if (w >= words) break;
-            const int64_t x = w * 32 + lane;
-            const bool in = x < R;
-            const bool c = in && row[x] >= sea;
-            const bool u = !in || !up || up[x] >= sea;
-            const bool d = !in || !dn || dn[x] >= sea;
-            const uint32_t bc = __ballot_sync(0xffffffffu, c);
-            const uint32_t bu = __ballot_sync(0xffffffffu, u);
-            const uint32_t bd = __ballot_sync(0xffffffffu, d);
-            if (lane == i) {
-                Lc = bc;
-                Lu = bu;
-                Ld = bd;
+        // two halves of 16 words: all 48 loads of a half are issued before the
+        // ballots (latency-bound otherwise); words past the row end read
+        // nothing (x >= R)
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float vc[16], vu[16], vd[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int64_t x = (w0 + 16 * half + i) * 32 + lane;
+                const bool in = x < R;
+                vc[i] = in ? row[x] : -INFINITY;
+                vu[i] = in && up ? up[x] : INFINITY;
+                vd[i] = in && dn ? dn[x] : INFINITY;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t bc = __ballot_sync(0xffffffffu, vc[i] >= sea);
+                const uint32_t bu = __ballot_sync(0xffffffffu, vu[i] >= sea);
+                const uint32_t bd = __ballot_sync(0xffffffffu, vd[i] >= sea);
+                if (lane == 16 * half + i) {
+                    Lc = bc;
+                    Lu = bu;
+                    Ld = bd;
+                }
             }
         }
         const int64_t w = w0 + lane;
@@ -206,11 +250,58 @@ __global__ void pack_mask_kernel(const uint8_t* __restrict__ m, int64_t R, uint3
     atomicAdd(&counts[1], pix);
 }
 
-// Occupied boxes of side eps (partial far-edge boxes count, analysis.hpp:284).
+__device__ __forceinline__ bool is_pow2_dev(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Power-of-two box sides on the packed coast bits: eps <= 32 is one thread per
+// (box row, 32-bit word) — OR of eps rows, then an OR-fold within each group
+// of eps bits and a popcount of the group leaders; eps > 32 is one thread per
+// box over eps rows x eps/32 words.  Bits past the row end are zero, so
+// partial far-edge boxes count as in analysis.hpp:284.
+__global__ void boxcount_pow2_kernel(const uint32_t* __restrict__ bits, int64_t R, int64_t rows,
+                                     const int32_t* sizes, int n_sizes, unsigned long long* __restrict__ out) {
+    const int s = blockIdx.y;
+    if (s >= n_sizes) return;
+    const int eps = sizes[s];
+    if (!is_pow2_dev(eps)) return;
+    const int64_t words = (R + 31) / 32;
+    const int64_t bpy = (rows + eps - 1) / eps;
+    unsigned long long occ = 0;
+    if (eps <= 32) {
+        const uint32_t lead = eps == 32 ? 1u : eps == 16 ? 0x00010001u : eps == 8 ? 0x01010101u
+                            : eps == 4 ? 0x11111111u : eps == 2 ? 0x55555555u : 0xFFFFFFFFu;
+        for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < bpy * words;
+             t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t by = t / words, w = t - by * words;
+            const int64_t y0 = by * eps, y1 = min(rows, y0 + eps);
+            uint32_t m = 0;
+            for (int64_t y = y0; y < y1; ++y) m |= __ldg(bits + y * words + w);
+            for (int sh = 1; sh < eps; sh <<= 1) m |= m >> sh;
+            occ += __popc(m & lead);
+        }
+    } else {
+        const int64_t wpb = eps / 32;
+        const int64_t bpx = (words + wpb - 1) / wpb;
+        for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < bpy * bpx;
+             t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t by = t / bpx, bx = t - by * bpx;
+            const int64_t y0 = by * eps, y1 = min(rows, y0 + eps);
+            const int64_t wa = bx * wpb, wb = min(words, wa + wpb);
+            uint32_t m = 0;
+            for (int64_t y = y0; y < y1 && !m; ++y)
+                for (int64_t w = wa; w < wb; ++w) m |= __ldg(bits + y * words + w);
+            occ += m ? 1 : 0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
+    if ((threadIdx.x & 31) == 0 && occ) atomicAdd(&out[s], occ);
+}
+
+// Occupied boxes of side eps (partial far-edge boxes count, analysis.hpp:284);
+// any side that is not a power of two.
 __global__ void boxcount_kernel(const uint32_t* __restrict__ bits, int64_t R, int64_t rows,
                                 const int32_t* sizes, int n_sizes, unsigned long long* __restrict__ out) {
     const int s = blockIdx.y;
-    if (s >= n_sizes) return;
+    if (s >= n_sizes || is_pow2_dev(sizes[s])) return;
     const int64_t eps = sizes[s];
     const int64_t words = (R + 31) / 32;
     const int64_t bpx = (R + eps - 1) / eps, bpy = (rows + eps - 1) / eps;
@@ -245,39 +336,127 @@ __global__ void boxcount_kernel(const uint32_t* __restrict__ bits, int64_t R, in
 
 // ---- variogram ----------------------------------------------------------------
 constexpr int kMaxLags = 32;
+constexpr int kFusedLags = 16;  // lags per fused pass (accumulators in registers)
 
-// Pairs whose first point lies in rows [0, P) of a W x H window (P = H for a
-// whole map; P < H when the rows below a band were regenerated as lookahead).
-__global__ void variogram_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld,
-                                 int64_t P, const int32_t* __restrict__ lags, int n_lags,
-                                 double* __restrict__ sums) {
-    // blockIdx.y = 2*lag + axis
-    const int q = blockIdx.y;
-    const int li = q >> 1, axis = q & 1;
-    const int64_t h = lags[li];
-    const int64_t nx = axis == 0 ? W - h : W;
-    const int64_t ny = axis == 0 ? P : min(P, H - h);
-    double acc = 0.0;
-    if (nx > 0 && ny > 0) {
-        const int64_t off = axis == 0 ? h : h * ld;
-        for (int64_t y = blockIdx.x; y < ny; y += gridDim.x) {
-            const float* row = z + y * ld;
-            for (int64_t x = threadIdx.x; x < nx; x += blockDim.x) {
-                // difference of two fp32 values is exact in fp64
-                const double d = static_cast<double>(row[x + off]) - static_cast<double>(row[x]);
-                acc = fma(d, d, acc);
+struct LagSet {
+    int n;
+    int h[kFusedLags];     // padded with 2^30 (never a pair)
+    int yoff[kFusedLags];  // h * ld, or -1: y-axis pairs done by variogram_y_kernel (h * ld >= 2^31)
+};
+
+constexpr int kSegC = 8192;    // columns per work item
+constexpr int kApron = 4096;   // x-lag partners beyond the segment kept in smem
+constexpr int kVgThreads = 256;
+
+// All (lag, axis) pairs of up to 16 lags in ONE pass over the map.  A work
+// item is (row y, column segment [x0, x0 + C)); the segment plus an apron of
+// up to 4096 columns is widened to fp64 once into shared memory, so every
+// x-lag pair is two shared loads + DADD + DFMA with no conversion; y-lag
+// partners z(x, y+h) are coalesced global loads (CTAs sweep consecutive rows
+// together, so partner rows of lags up to a few hundred are L2 hits).  The
+// difference of two fp32 values is exact in fp64; sums are fp64.  Pairs whose
+// first point lies in rows [0, P) of a W x H window (P = H for a whole map;
+// P < H when the rows below a band were regenerated as lookahead).
+// sums[2*l + axis].
+// NL: lags in this pass (the set is padded to NL); kLongX: some x-lag exceeds
+// the apron (its partners are read from global memory).
+template <int NL, bool kLongX>
+__global__ void __launch_bounds__(kVgThreads, 2)
+variogram_seg_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld, int64_t P,
+                     const __grid_constant__ LagSet L, int64_t nseg, int seg_cap,
+                     double* __restrict__ sums) {
+    extern __shared__ double seg[];
+    double ax[NL], ay[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) ax[l] = ay[l] = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t items = P * nseg;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t y = it / nseg;
+        const int64_t x0 = (it - y * nseg) * kSegC;
+        const int wl = static_cast<int>(W - x0);                              // columns from x0
+        const int hl = static_cast<int>(H - y < (1 << 30) ? H - y : (1 << 30));  // rows from y
+        const int cw = wl < kSegC ? wl : kSegC;
+        const int sw = wl < seg_cap ? wl : seg_cap;  // segment + apron
+        const float* row = z + y * ld + x0;
+        int yo[NL];  // per-item partner offsets; 0 (partner = self, d = 0) where no pair
+#pragma unroll
+        for (int l = 0; l < NL; ++l) yo[l] = (L.yoff[l] >= 0 && L.h[l] < hl) ? L.yoff[l] : 0;
+        __syncthreads();  // previous item's readers are done with seg
+        for (int i = threadIdx.x; i < sw; i += kVgThreads) seg[i] = static_cast<double>(__ldg(row + i));
+        __syncthreads();
+        for (int xb = warp * 128; xb < cw; xb += (kVgThreads / 32) * 128) {
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) {
+                const int x = xb + 32 * j + lane;
+                if (x >= cw) break;
+                const float* rp = row + x;
+                float py[NL];
+#pragma unroll
+                for (int l = 0; l < NL; ++l) py[l] = __ldg(rp + yo[l]);
+                const double v = seg[x];
+#pragma unroll
+                for (int l = 0; l < NL; ++l) {
+                    const int h = L.h[l];
+                    if (x + h < wl) {
+                        // without kLongX every h <= kApron, so x + h < sw: in smem
+                        const double p = (kLongX && x + h >= sw) ? static_cast<double>(__ldg(rp + h)) : seg[x + h];
+                        const double d = p - v;
+                        ax[l] = fma(d, d, ax[l]);
+                    }
+                    const double d = static_cast<double>(py[l]) - v;
+                    ay[l] = fma(d, d, ay[l]);
+                }
             }
+        }
+    }
+    __syncthreads();
+    double* part = seg;  // [8 warps][32]
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        double a = ax[l], b = ay[l];
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0) {
+            part[warp * 2 * kFusedLags + 2 * l] = a;
+            part[warp * 2 * kFusedLags + 2 * l + 1] = b;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * L.n) {
+        double t = 0.0;
+        for (int w = 0; w < kVgThreads / 32; ++w) t += part[w * 2 * kFusedLags + threadIdx.x];
+        atomicAdd(&sums[threadIdx.x], t);
+    }
+}
+
+// y-axis pairs of lags whose row offset h * ld does not fit 32 bits
+// (blockIdx.y = entry of `which`), one fp64 partial per block.
+__global__ void variogram_y_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld, int64_t P,
+                                   const __grid_constant__ LagSet L, double* __restrict__ sums) {
+    const int l = blockIdx.y;
+    if (L.yoff[l] >= 0) return;  // done by the fused kernel
+    const int64_t h = L.h[l];
+    const int64_t ny = min(P, H - h);
+    double acc = 0.0;
+    for (int64_t y = blockIdx.x; y < ny; y += gridDim.x) {
+        const float* a = z + y * ld;
+        const float* b = a + h * ld;
+        for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
+            const double d = static_cast<double>(b[x]) - static_cast<double>(a[x]);
+            acc = fma(d, d, acc);
         }
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     __shared__ double part[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) part[warp] = acc;
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (warp == 0) {
-        acc = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) atomicAdd(&sums[q], acc);
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
+        atomicAdd(&sums[2 * l + 1], t);
     }
 }
 
@@ -304,19 +483,17 @@ int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* str
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Scratch scr(s);
-    const size_t part_bytes = static_cast<size_t>(kHistBlocks) * kBins * sizeof(unsigned int);
-    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long) + part_bytes);
+    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long));
     if (e != cudaSuccess) return set_cuda_error(e, "median alloc");
     SelectState* state = static_cast<SelectState*>(scr.p);
     unsigned long long* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);
-    unsigned int* partials = reinterpret_cast<unsigned int*>(hist + kBins);
     SelectState init{0u, 0u, n / 2};  // analysis.hpp:247 (upper median)
     e = cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned long long), s);
     const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
     for (int p = 0; p < 3 && e == cudaSuccess; ++p) {
-        radix_hist<<<kHistBlocks, 512, 0, s>>>(dev_map, n, state, shifts[p], widths[p], partials);
-        hist_reduce<<<kBins / 256, 256, 0, s>>>(partials, kHistBlocks, hist);
-        radix_pick<<<1, 32, 0, s>>>(state, hist, shifts[p], widths[p]);
+        radix_hist<<<kHistBlocks, 512, 0, s>>>(dev_map, n, state, shifts[p], widths[p], hist);
+        radix_pick<<<1, kBins / 2, 0, s>>>(state, hist, shifts[p], widths[p]);
         e = cudaGetLastError();
     }
     SelectState res{};
@@ -358,8 +535,11 @@ static int boxcount_from_bits(const uint32_t* bits, int64_t R, int64_t rows, con
                               unsigned long long* dcounts, int32_t* dsizes, cudaStream_t s) {
     cudaError_t e = cudaMemcpyAsync(dsizes, sizes, n * sizeof(int32_t), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return set_cuda_error(e, "boxcount sizes");
-    dim3 grid(148 * 2, static_cast<unsigned>(n));
-    boxcount_kernel<<<grid, 256, 0, s>>>(bits, R, rows, dsizes, n, dcounts);
+    dim3 grid(148 * 4, static_cast<unsigned>(n));
+    bool any_other = false;
+    for (int i = 0; i < n; ++i) any_other = any_other || (sizes[i] & (sizes[i] - 1)) != 0;
+    boxcount_pow2_kernel<<<grid, 256, 0, s>>>(bits, R, rows, dsizes, n, dcounts);
+    if (any_other) boxcount_kernel<<<grid, 256, 0, s>>>(bits, R, rows, dsizes, n, dcounts);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "boxcount launch");
     return TG_OK;
@@ -484,16 +664,60 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Scratch scr(s);
-    cudaError_t e = scr.alloc(2 * kMaxLags * sizeof(double) + kMaxLags * sizeof(int32_t));
+    cudaError_t e = scr.alloc(2 * kMaxLags * sizeof(double));
     if (e != cudaSuccess) return set_cuda_error(e, "variogram alloc");
     auto* sums = static_cast<double*>(scr.p);
-    auto* dl = reinterpret_cast<int32_t*>(sums + 2 * kMaxLags);
     e = cudaMemsetAsync(sums, 0, 2 * kMaxLags * sizeof(double), s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dl, lags, n_lags * sizeof(int32_t), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return set_cuda_error(e, "variogram setup");
-    dim3 grid(148 * 2, static_cast<unsigned>(2 * n_lags));
-    variogram_kernel<<<grid, 256, 0, s>>>(dev_map, width, height, ld, pair_rows, dl, n_lags, sums);
-    e = cudaGetLastError();
+    int sm = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t nseg = (width + kSegC - 1) / kSegC;
+    const int seg_cap = static_cast<int>(std::min<int64_t>(width, kSegC + kApron));
+    const size_t smem = std::max<size_t>(static_cast<size_t>(seg_cap), 2 * kFusedLags * (kVgThreads / 32)) * sizeof(double);
+    static bool attr_set = false;  // >48 KiB dynamic smem opt-in (idempotent)
+    if (!attr_set) {
+        const int mx = static_cast<int>((kSegC + kApron) * sizeof(double));
+        for (auto f : {variogram_seg_kernel<4, false>, variogram_seg_kernel<8, false>, variogram_seg_kernel<12, false>,
+                       variogram_seg_kernel<16, false>, variogram_seg_kernel<4, true>, variogram_seg_kernel<8, true>,
+                       variogram_seg_kernel<12, true>, variogram_seg_kernel<16, true>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        attr_set = true;
+    }
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, 2 * static_cast<int64_t>(sm)));
+    // passes of <= 12 lags, balanced (13 lags -> 7 + 6: the 16-lag variant
+    // runs out of registers)
+    const int passes = (n_lags + 11) / 12, per_pass = (n_lags + passes - 1) / passes;
+    for (int l0 = 0; l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += per_pass) {
+        LagSet L{};
+        L.n = std::min(per_pass, n_lags - l0);
+        bool long_x = false, long_y = false;
+        for (int i = 0; i < kFusedLags; ++i) {
+            const int64_t h = i < L.n ? lags[l0 + i] : 0;
+            const bool pad = i >= L.n || h >= (int64_t(1) << 30);  // >= 2^30: no pair on either axis
+            L.h[i] = pad ? (1 << 30) : static_cast<int>(h);
+            const bool wide = !pad && h * ld >= (int64_t(1) << 31);
+            L.yoff[i] = pad ? 0 : wide ? -1 : static_cast<int>(h * ld);
+            long_x = long_x || (!pad && h > kApron);
+            long_y = long_y || (wide && h < height);
+        }
+        if (long_y) {
+            variogram_y_kernel<<<dim3(2 * sm, static_cast<unsigned>(L.n)), 256, 0, s>>>(
+                dev_map, width, height, ld, pair_rows, L, sums + 2 * l0);
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+        }
+        using K = void (*)(const float*, int64_t, int64_t, int64_t, int64_t, LagSet, int64_t, int, double*);
+        static const K table[2][4] = {
+            {variogram_seg_kernel<4, false>, variogram_seg_kernel<8, false>, variogram_seg_kernel<12, false>,
+             variogram_seg_kernel<16, false>},
+            {variogram_seg_kernel<4, true>, variogram_seg_kernel<8, true>, variogram_seg_kernel<12, true>,
+             variogram_seg_kernel<16, true>}};
+        table[long_x ? 1 : 0][(L.n - 1) / 4]<<<static_cast<unsigned>(blocks), kVgThreads, smem, s>>>(
+            dev_map, width, height, ld, pair_rows, L, nseg, seg_cap, sums + 2 * l0);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_sum_sq, sums, 2 * n_lags * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return set_cuda_error(e, "variogram");
@@ -522,22 +746,20 @@ int tg_histogram_f32(const float* dev_rows, int64_t width, int64_t rows, int64_t
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Scratch scr(s);
-    const size_t part_bytes = static_cast<size_t>(kHistBlocks) * kBins * sizeof(unsigned int);
-    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long) + part_bytes);
+    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long));
     if (e != cudaSuccess) return set_cuda_error(e, "histogram alloc");
     SelectState* state = static_cast<SelectState*>(scr.p);
     auto* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);
-    unsigned int* partials = reinterpret_cast<unsigned int*>(hist + kBins);
     SelectState init{prefix, mask, 0};
     e = cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned long long), s);
     const int blocks = static_cast<int>(std::min<int64_t>(rows, kHistBlocks));
     if (e == cudaSuccess) {
         if (ld == width)
             radix_hist<<<kHistBlocks, 512, 0, s>>>(dev_rows, static_cast<uint64_t>(width * rows), state, shift, bits,
-                                                   partials);
+                                                   hist);
         else
-            radix_hist2d<<<blocks, 512, 0, s>>>(dev_rows, width, rows, ld, state, shift, bits, partials);
-        hist_reduce<<<kBins / 256, 256, 0, s>>>(partials, ld == width ? kHistBlocks : blocks, hist);
+            radix_hist2d<<<blocks, 512, 0, s>>>(dev_rows, width, rows, ld, state, shift, bits, hist);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess)

@@ -344,7 +344,9 @@ def test_box_count_known_answers():
 
 
 @pytest.mark.parametrize("R,sizes", [(512, [2, 4, 8, 16, 32, 64]), (1000, [3, 5, 7, 33, 100]),
-                                     (4096, [2, 4, 8, 16, 32, 64])])
+                                     (4096, [2, 4, 8, 16, 32, 64]),
+                                     (1000, [1, 2, 3, 4, 8, 16, 32, 64, 128, 256, 500]),
+                                     (777, [2, 4, 8, 16, 32, 64, 128])])
 def test_fused_boxcount_matches_oracle(oracle, R, sizes):
     c = make_cfg(method=0, smoothstep=5, seed=42, resolution=R, base_frequency=8, octaves=8)
     m = gen(c, 0, 0, R)
@@ -363,6 +365,55 @@ def test_variogram_matches_oracle(oracle):
     m = gen(c, 0, 0, 512)
     lags = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
     ss, pr = pt.variogram_device(m, 512, 512, lags)
+    rss, rpr = oracle.variogram(m.cpu().numpy().astype(np.float64), lags)
+    assert np.array_equal(pr, rpr)
+    assert np.allclose(ss, rss, rtol=1e-10, atol=0)
+
+
+def test_variogram_special_values(oracle):
+    """Zeros, signed zeros and subnormals take the hardware fp32->fp64 path."""
+    g = torch.Generator().manual_seed(4)
+    m = torch.randn((64, 300), generator=g)
+    m[::3, ::5] = 0.0
+    m[1::7, ::3] = -0.0
+    m[2::5, 1::4] = 1e-40
+    m[3::9, 2::6] = -3e-42
+    m[5, :] = 3.0e38
+    dev = m.cuda()
+    lags = [1, 2, 3, 5, 8, 13, 21, 34, 55]
+    ss, pr = pt.variogram_device(dev, 300, 64, lags)
+    rss, rpr = oracle.variogram(m.numpy().astype(np.float64), lags)
+    assert np.array_equal(pr, rpr)
+    assert np.allclose(ss, rss, rtol=1e-10, atol=0)
+
+
+def test_variogram_row_offsets_beyond_32_bits(oracle):
+    """h * ld >= 2^31: the y-axis of that lag is summed by the wide-offset kernel."""
+    H, W, ld = 1100, 64, 1 << 21
+    big = torch.empty((H, ld), dtype=torch.float32, device="cuda")  # 9.2 GB, only W columns touched
+    g = torch.Generator().manual_seed(8)
+    m = torch.randn((H, W), generator=g)
+    big[:, :W] = m.cuda()
+    lags = [1, 3, 1023, 1024, 1099, 1100]
+    arr = (C.c_int32 * len(lags))(*lags)
+    ss = (C.c_double * (2 * len(lags)))()
+    pr = (C.c_int64 * (2 * len(lags)))()
+    assert _abi.load().tg_variogram_f32(big.data_ptr(), W, H, ld, arr, len(lags), ss, pr, None) == 0
+    rss, rpr = oracle.variogram(m.numpy().astype(np.float64), lags)
+    assert np.array_equal(np.array(pr[:]).reshape(-1, 2), rpr)
+    assert np.allclose(np.array(ss[:]).reshape(-1, 2), rss, rtol=1e-10, atol=0)
+    del big
+
+
+@pytest.mark.parametrize("W,H,lags", [
+    (700, 300, [1, 3, 7, 100, 299, 300, 650]),                   # ragged, lags >= H, 7 -> padded to 8
+    (9000, 40, [1, 2, 4096, 4097, 5000, 8999, 9000]),            # segments + apron, x-lags beyond the apron
+    (257, 129, list(range(1, 21))),                              # 20 lags: two passes (16 + 4)
+])
+def test_variogram_segments_and_lag_sets(oracle, W, H, lags):
+    c = make_cfg(method=0, smoothstep=5, seed=9, resolution=16384, base_frequency=32, octaves=12)
+    m = gen(c, 0, 0, W, H)
+    ss, pr = pt.variogram_device(m, W, H, lags)
     rss, rpr = oracle.variogram(m.cpu().numpy().astype(np.float64), lags)
     assert np.array_equal(pr, rpr)
     assert np.allclose(ss, rss, rtol=1e-10, atol=0)
