@@ -272,10 +272,13 @@ __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRP
 #ifndef TG_ZG_MIN_BLOCKS
 #define TG_ZG_MIN_BLOCKS 3
 #endif
+#ifndef TG_GEN_MIN_BLOCKS
+#define TG_GEN_MIN_BLOCKS 1
+#endif
 
 template <int KIND, int ORDER>
 __global__ void __launch_bounds__(kThreads, (KIND == kZgPaper || KIND == kZgSeparable) ? TG_ZG_MIN_BLOCKS
-                                            : (KIND == kPerlin ? 2 : 1))
+                                            : (KIND == kPerlin ? 2 : TG_GEN_MIN_BLOCKS))
 fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     constexpr int CH = Traits<KIND>::kCh;
     constexpr bool kZg = KIND == kZgPaper || KIND == kZgSeparable;

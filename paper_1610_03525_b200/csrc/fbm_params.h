@@ -66,6 +66,7 @@ struct OctDev {
     int32_t tslot;     // sampling-table slot (kModeGrid) or -1
     int32_t lut_off;   // offset of this ppc's row LUT (aligned modes) or -1
     int32_t pad;
+    double ratio;      // freq / R (OpenSimplex sample spacing), set by its launcher
 };
 
 // Octave lists built by the host planner (capi.cu): the kernel loops over

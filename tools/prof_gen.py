@@ -16,6 +16,8 @@ CONFIGS = {
     "cfg1": (dict(seed=1, resolution=1024, base_frequency=8, octaves=8), 1024),
     "cfg2": (dict(seed=1, smoothstep=5, resolution=4096, base_frequency=8, octaves=12), 4096),
     "cfg3p": (dict(seed=1, method=pt.Method.perlin3, resolution=4096, base_frequency=8, octaves=12), 4096),
+    "cfg3s": (dict(seed=1, method=pt.Method.opensimplex, resolution=4096, base_frequency=8, octaves=12), 4096),
+    "cfg3g": (dict(seed=1, method=pt.Method.generic, resolution=4096, base_frequency=8, octaves=12), 4096),
     "cfg5": (dict(seed=1, smoothstep=5, resolution=32768, base_frequency=32, octaves=16), 4096),
 }
 
