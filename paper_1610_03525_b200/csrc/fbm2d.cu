@@ -622,8 +622,17 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                     last = ry;
                 }
                 const auto row = cell.row(f.x, f.y);
+                if constexpr (KIND == kPerlin) {
+                    // the column-independent term goes to the row accumulator:
+                    // 3 FFMA per pixel
+                    racc[r] += row.a0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
+                    for (int j = 0; j < 4; ++j)
+                        acc[r][j] = fmaf(xs[j], row.a3, fmaf(sx[j], row.a2, fmaf(x[j], row.a1, acc[r][j])));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
+                }
             }
             continue;
         }
