@@ -246,17 +246,20 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch
 
 // zero-gradient cell rows r_begin.. of one cell: c0 = h00 + sy*dy goes into
 // the per-row accumulator (common to the 4 columns), the rest per pixel.
-template <int KIND, int NR>
-__device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRPT], int r_begin,
+template <int KIND, int NR, bool ONE_CELL = false>
+__device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRPT], float& hsum, int r_begin,
                                         const float4* __restrict__ Ly, const float (&x)[4],
                                         const float (&sx)[4], float h00, float h10, float h01,
                                         float h11) {
     const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+    // ONE_CELL: h00 is common to every pixel of the thread -> one add per octave
+    if constexpr (ONE_CELL) hsum += h00;
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
         const int r = r_begin + rr;
         const float4 f = Ly[rr];
-        racc[r] += fmaf(f.y, dy, h00);
+        if constexpr (ONE_CELL) racc[r] = fmaf(f.y, dy, racc[r]);
+        else racc[r] += fmaf(f.y, dy, h00);
         if constexpr (KIND == kZgPaper) {
             const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
 #pragma unroll
@@ -269,6 +272,9 @@ __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRP
     }
 }
 
+#ifndef TG_HSUM
+#define TG_HSUM true
+#endif
 #ifndef TG_ZG_MIN_BLOCKS
 #define TG_ZG_MIN_BLOCKS 3
 #endif
@@ -413,6 +419,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     // ---- evaluation of the thread's 4 x 8 pixels (no barriers) --------------
     float acc[kRPT][4];
     float racc[kRPT];  // per-row terms common to the 4 columns (zg block modes)
+    float hsum = 0.f;  // term common to all 32 pixels (zg block modes)
 #pragma unroll
     for (int r = 0; r < kRPT; ++r) {
         racc[r] = 0.f;
@@ -437,7 +444,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 x[j] = e.x;
                 sx[j] = e.y;
             }
-            zg_rows<KIND, kRPT>(acc, racc, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
+            zg_rows<KIND, kRPT, TG_HSUM>(acc, racc, hsum, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
                              amp * g[od.pitch + 1]);
         }
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
@@ -456,10 +463,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             }
             const float a0 = amp * g[0], a1 = amp * g[1];
             const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
-            zg_rows<KIND, 4>(acc, racc, 0, L, x, sx, a0, a1, b0, b1);
+            zg_rows<KIND, 4>(acc, racc, hsum, 0, L, x, sx, a0, a1, b0, b1);
             if constexpr (kRPT == 8) {
                 const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
-                zg_rows<KIND, 4>(acc, racc, 4, L, x, sx, b0, b1, e0, e1);
+                zg_rows<KIND, 4>(acc, racc, hsum, 4, L, x, sx, b0, b1, e0, e1);
             }
         }
     }
@@ -469,7 +476,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] += racc[r];
+            for (int j = 0; j < 4; ++j) acc[r][j] += racc[r] + hsum;
             racc[r] = 0.f;
         }
     }
