@@ -272,6 +272,9 @@ __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRP
     }
 }
 
+#ifndef TG_TMA_STORE
+#define TG_TMA_STORE 1
+#endif
 #ifndef TG_HSUM
 #define TG_HSUM true
 #endif
@@ -761,6 +764,49 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     // ---- single fp32 store of the finished tile ----------------------------
     const int64_t lx0 = tx0 + c0 - args.ox;
     const int64_t ly0 = ty0 + r0 - args.oy;
+#if TG_TMA_STORE
+    // Interior tiles: stage the 128 x 64 tile in shared memory (the corner
+    // grids are dead by now) and let the bulk-copy engine write each 512-byte
+    // row to HBM (cp.async.bulk, one lane per warp for the warp's 8 rows).
+    const bool tile_full = tx0 - args.ox >= 0 && tx0 - args.ox + kTW <= args.width && ty0 - args.oy >= 0 &&
+                           ty0 - args.oy + kTH <= args.height && ((tx0 - args.ox) & 3) == 0 &&
+                           (args.ld & 3) == 0 && (args.map_stride & 3) == 0 &&
+                           (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    if (tile_full) {  // uniform per CTA
+        __syncthreads();  // every warp is done reading the corner grids
+        float* stage = grid;
+#pragma unroll
+        for (int r = 0; r < kRPT; ++r) {
+            float w[4] = {acc[r][0] + racc[r], acc[r][1] + racc[r], acc[r][2] + racc[r], acc[r][3] + racc[r]};
+            if (args.epilogue) {
+                const float invR = static_cast<float>(1.0 / args.R);
+                const float vv = (static_cast<float>(ty0 + r0 + r) + 0.5f) * invR;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float u = (static_cast<float>(tx0 + c0 + j) + 0.5f) * invR;
+                    const float phase =
+                        args.epilogue == 1 ? u : sqrtf((u - 0.5f) * (u - 0.5f) + (vv - 0.5f) * (vv - 0.5f));
+                    w[j] = sinf(fmaf(args.tex_freq2pi, phase, args.tex_gain * w[j]));
+                }
+            }
+            *reinterpret_cast<float4*>(stage + (r0 + r) * kTW + c0) = make_float4(w[0], w[1], w[2], w[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            float* grow = out + static_cast<int64_t>(blockIdx.z) * args.map_stride + ly0 * args.ld + (tx0 - args.ox);
+            const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(stage + r0 * kTW));
+#pragma unroll
+            for (int r = 0; r < kRPT; ++r)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(grow + r * args.ld),
+                             "r"(s0 + r * kTW * 4), "n"(kTW * 4)
+                             : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        return;
+    }
+#endif
     float* row = out + static_cast<int64_t>(blockIdx.z) * args.map_stride + ly0 * args.ld + lx0;
     const bool vec_ok = ((lx0 & 3) == 0) && ((args.ld & 3) == 0) && ((args.map_stride & 3) == 0) &&
                         ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && lx0 >= 0 &&
