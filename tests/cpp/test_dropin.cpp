@@ -239,6 +239,32 @@ int main() {
         const auto rows = analysis::dimension_vs_octaves(cfg, 1, 3, ps, analysis::default_box_sizes());
         EXPECT(rows.size() == 3u && rows[2].octaves == 3, "sweep rows");
     }
+    // acceptance_tests.cpp:384-436 (criterion 10): box-counting dimension
+    // windows and the octave / persistence trends, through the drop-in
+    {
+        const auto measure = [](int octaves, double persistence) {
+            FbmConfig cfg;
+            cfg.seed = 42;
+            cfg.resolution = 512;
+            cfg.octaves = octaves;
+            cfg.persistence = persistence;
+            return analysis::box_count(generate_heightmap(cfg));
+        };
+        const auto headline = measure(8, 0.5);
+        EXPECT(headline.d > 1.0 && headline.d < 2.0 && headline.r2 > 0.98, "512^2 p=0.5 N=8 D window, r2");
+        double prev = 0.0;
+        bool mono = true;
+        for (int n = 1; n <= 8; ++n) {
+            const double d = measure(n, 0.5).d;
+            if (n > 1) mono = mono && d >= prev - 0.05;
+            prev = d;
+        }
+        EXPECT(mono, "D(N) non-decreasing within 0.05");
+        const double d3 = measure(8, 0.3).d, d5 = measure(8, 0.5).d, d7 = measure(8, 0.7).d;
+        EXPECT(d5 >= d3 - 0.05 && d7 >= d5 - 0.05, "D grows with persistence");
+        std::printf("criterion 10: D=%.4f r2=%.5f; D(p=.3/.5/.7)=%.3f %.3f %.3f\n", headline.d, headline.r2, d3,
+                    d5, d7);
+    }
     // PGM16 / PNG16 export of a device map (compared byte-for-byte with the
     // reference writers by tests/test_cpp_dropin.py)
     {
