@@ -173,6 +173,38 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": rs, "samples": len(self.samples)}
 
 
+def hashes_per_launch(res: int, f0: int, octaves: int, tw: int = 128, th: int = 64) -> int:
+    """Lattice-corner hashes one config-2-shaped launch performs: every
+    octave's corner grid per 128 x 64 tile (shared by the tile's pixels), one
+    hash per pixel for the lattice-point (sub-pixel) octaves."""
+    tiles = (res // tw) * (res // th)
+    total = 0
+    for o in range(octaves):
+        freq = f0 * 2 ** o
+        if freq > res:
+            total += res * res
+            continue
+        ppc = res // freq
+        nx = tw // ppc + 1 if ppc <= tw else 2
+        ny = th // ppc + 1 if ppc <= th else 2
+        total += tiles * nx * ny
+    return total
+
+
+def measured_hbm_gbs() -> float:
+    """HBM bandwidth from the driver-written MEASURED_PEAKS.json, else the
+    B200 profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k in ("hbm_gbs", "hbm_copy_gbs", "hbm_bw_gbs"):
+            if isinstance(d.get(k), (int, float)):
+                return float(d[k])
+    except Exception:
+        pass
+    return 6458.4
+
+
 def traffic_summary():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -378,7 +410,11 @@ def main() -> None:
                                   f"x {int(so_per_step)} sample-octaves per launch / mean CUDA-event launch "
                                   f"time {avg_launch_s*1e6:.1f} us; peak = FFMA-chain measured in-run "
                                   f"(MEASURED_PEAKS.json has no FP32 entry)"),
-                         "hbm_write_gbs": hbm_gbs, "hbm_frac": hbm_gbs / 6458.4,
+                         "hbm_write_gbs": hbm_gbs, "hbm_frac": hbm_gbs / measured_hbm_gbs(),
+                         "hashes_per_launch": hashes_per_launch(R, F0, OCTAVES),
+                         "hashes_per_s": hashes_per_launch(R, F0, OCTAVES) / avg_launch_s,
+                         "pipes_pct_ncu": {k: (traffic_summary() or {}).get(k)
+                                           for k in ("pipe_fma_pct", "pipe_alu_pct", "pipe_xu_pct")},
                          "issue_slots_busy_pct_ncu": (traffic_summary() or {}).get("issue_active_pct"),
                          "issue_note": "the bit-exact 64-bit lattice hash is integer work outside the 7-flop "
                                        "convention; issue-slot utilisation of the same kernel from the committed "
