@@ -368,7 +368,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
         const int pitch = od.pitch;
         const uint64_t p0 = pack_xy(base, ix0, iy0);
         float* g = grid + od.goff;
-        if (kZg && aligned && od.shift <= 4) {
+        if (aligned && od.shift <= 4) {
             // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc.  The main
             // block goes 4 consecutive corners per lane (four independent hash
             // chains, keys advanced by +K3, one 16-byte store); the last column
@@ -381,15 +381,29 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
             for (int cy = (warp << sh) + rs; cy < Hm; cy += rstep) {
                 const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
-                float h[4];
-                height_scaled4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
-                *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
+                if constexpr (kZg) {
+                    float h[4];
+                    height_scaled4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
+                    *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
+                } else {
+                    float d[4][CH];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) grid_value(add64(p, u * kIxMul), od, d[u]);
+#pragma unroll
+                    for (int c = 0; c < CH; ++c)
+                        *reinterpret_cast<float4*>(g + c * kGridCap + cy * pitch + 4 * cg) =
+                            make_float4(d[0][c], d[1][c], d[2][c], d[3][c]);
+                }
             }
             for (int i = tid; i < Hm + 1 + Wm; i += kThreads) {
                 const int cx = i <= Hm ? Wm : i - Hm - 1;
                 const int cy = i <= Hm ? i : Hm;
-                g[cy * pitch + cx] = height_scaled(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
-                                                   static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul);
+                float d[CH];
+                grid_value(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                               static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul,
+                           od, d);
+#pragma unroll
+                for (int c = 0; c < CH; ++c) g[c * kGridCap + cy * pitch + cx] = d[c];
             }
         } else {
             // Any other shape: flat corner list, four hash chains per thread.
