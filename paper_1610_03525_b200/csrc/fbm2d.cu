@@ -635,37 +635,57 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 sx[j] = e.y;
                 xs[j] = e.w;
             }
-            Cell<KIND> cell;
-            int last = -1;
-#pragma unroll
-            for (int r = 0; r < kRPT; ++r) {
-                const int yr = yo + r;
-                const int ry = yr >> sh;
-                const float4 f = L[yr & mask];
-                if (ry != last) {
-                    const int key = ry * pitch;
-                    float k00[CH], k10[CH], k01[CH], k11[CH];
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        k00[c] = gscale * g[c * kGridCap + key];
-                        k10[c] = gscale * g[c * kGridCap + key + 1];
-                        k01[c] = gscale * g[c * kGridCap + key + pitch];
-                        k11[c] = gscale * g[c * kGridCap + key + pitch + 1];
-                    }
-                    cell.make(k00, k10, k01, k11);
-                    last = ry;
-                }
-                const auto row = cell.row(f.x, f.y);
+            // row terms: the column-independent one to the row accumulator,
+            // the rest 3 FFMA per pixel (Perlin {x, sx, xs}, generic Horner in x)
+            auto accum = [&](int r, const typename Cell<KIND>::Row& row) {
                 if constexpr (KIND == kPerlin) {
-                    // the column-independent term goes to the row accumulator:
-                    // 3 FFMA per pixel
                     racc[r] += row.a0;
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         acc[r][j] = fmaf(xs[j], row.a3, fmaf(sx[j], row.a2, fmaf(x[j], row.a1, acc[r][j])));
+                } else if constexpr (KIND == kGeneric) {
+                    racc[r] += row.r0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        acc[r][j] = fmaf(fmaf(fmaf(row.r3, x[j], row.r2), x[j], row.r1), x[j], acc[r][j]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
+                }
+            };
+            auto load_cell = [&](Cell<KIND>& cell, int ry) {
+                const int key = ry * pitch;
+                float k00[CH], k10[CH], k01[CH], k11[CH];
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    k00[c] = gscale * g[c * kGridCap + key];
+                    k10[c] = gscale * g[c * kGridCap + key + 1];
+                    k01[c] = gscale * g[c * kGridCap + key + pitch];
+                    k11[c] = gscale * g[c * kGridCap + key + pitch + 1];
+                }
+                cell.make(k00, k10, k01, k11);
+            };
+            Cell<KIND> cell;
+            if (od.ppc >= kRPT) {
+                // the thread's rows lie in one cell: corners once per octave
+                load_cell(cell, yo >> sh);
+#pragma unroll
+                for (int r = 0; r < kRPT; ++r) {
+                    const float4 f = L[(yo + r) & mask];
+                    accum(r, cell.row(f.x, f.y));
+                }
+            } else {
+                int last = -1;
+#pragma unroll
+                for (int r = 0; r < kRPT; ++r) {
+                    const int yr = yo + r;
+                    const int ry = yr >> sh;
+                    const float4 f = L[yr & mask];
+                    if (ry != last) {
+                        load_cell(cell, ry);
+                        last = ry;
+                    }
+                    accum(r, cell.row(f.x, f.y));
                 }
             }
             continue;
