@@ -88,7 +88,9 @@ struct Smem3 {
     float grid[kCap3];
 };
 
-template <int ORDER>
+// LEAN: no general octaves in the plan (host-decided): the per-voxel general
+// path is compiled out, which lowers the register pressure of the rest.
+template <int ORDER, bool LEAN>
 __global__ void __launch_bounds__(kThreads3, 2)
 fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char raw3[];
@@ -323,6 +325,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         }
 
         // general octaves: per-voxel cell lookup (grid or hashed corners)
+        if constexpr (LEAN) continue;
         const bool direct = mode == kM3Direct;
         float sx[4];
         int64_t ixj[4];
@@ -400,11 +403,11 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     }
 }
 
-template <int ORDER>
-cudaError_t launch3(const Fbm3Args& a, float* out, cudaStream_t st) {
+template <int ORDER, bool LEAN>
+cudaError_t launch3v(const Fbm3Args& a, float* out, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fbm3d_kernel<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(fbm3d_kernel<ORDER, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sizeof(Smem3)));
         if (e != cudaSuccess) return e;
         configured = true;
@@ -412,8 +415,15 @@ cudaError_t launch3(const Fbm3Args& a, float* out, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>((a.ox + a.nx - a.tile_x0 + kTX - 1) / kTX),
               static_cast<unsigned>((a.oy + a.ny - a.tile_y0 + kTY - 1) / kTY),
               static_cast<unsigned>((a.oz + a.nz - a.tile_z0 + kTZ - 1) / kTZ));
-    fbm3d_kernel<ORDER><<<grid, kThreads3, sizeof(Smem3), st>>>(a, out);
+    fbm3d_kernel<ORDER, LEAN><<<grid, kThreads3, sizeof(Smem3), st>>>(a, out);
     return cudaGetLastError();
+}
+
+template <int ORDER>
+cudaError_t launch3(const Fbm3Args& a, float* out, cudaStream_t st) {
+    bool lean = true;
+    for (int o = 0; o < a.octaves; ++o) lean = lean && a.oct[o].mode != kM3Gen && a.oct[o].mode != kM3Direct;
+    return lean ? launch3v<ORDER, true>(a, out, st) : launch3v<ORDER, false>(a, out, st);
 }
 
 }  // namespace
