@@ -247,7 +247,10 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch
 
 // zero-gradient cell rows r_begin.. of one cell: c0 = h00 + sy*dy goes into
 // the per-row accumulator (common to the 4 columns), the rest per pixel.
-template <int KIND, int NR, bool ONE_CELL = false>
+// DIRECT_C0 (lean paper kernel): the column-independent term is added per
+// pixel instead of through the row accumulators, whose 8 registers the
+// 4-CTA/SM (64-register) lean kernel cannot afford.
+template <int KIND, int NR, bool ONE_CELL = false, bool DIRECT_C0 = false>
 __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRPT], float& hsum, int r_begin,
                                         const float4* __restrict__ Ly, const float (&x)[4],
                                         const float (&sx)[4], float h00, float h10, float h01,
@@ -259,6 +262,13 @@ __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRP
     for (int rr = 0; rr < NR; ++rr) {
         const int r = r_begin + rr;
         const float4 f = Ly[rr];
+        if constexpr (DIRECT_C0 && KIND == kZgPaper) {
+            const float c0 = ONE_CELL ? f.y * dy : fmaf(f.y, dy, h00);
+            const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j] + c0));
+            continue;
+        }
         if constexpr (ONE_CELL) racc[r] = fmaf(f.y, dy, racc[r]);
         else racc[r] += fmaf(f.y, dy, h00);
         if constexpr (KIND == kZgPaper) {
@@ -469,7 +479,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 x[j] = e.x;
                 sx[j] = e.y;
             }
-            zg_rows<KIND, kRPT, TG_HSUM>(acc, racc, hsum, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
+            zg_rows<KIND, kRPT, TG_HSUM, LEAN>(acc, racc, hsum, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
                              amp * g[od.pitch + 1]);
         }
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
@@ -488,10 +498,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             }
             const float a0 = amp * g[0], a1 = amp * g[1];
             const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
-            zg_rows<KIND, 4>(acc, racc, hsum, 0, L, x, sx, a0, a1, b0, b1);
+            zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 0, L, x, sx, a0, a1, b0, b1);
             if constexpr (kRPT == 8) {
                 const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
-                zg_rows<KIND, 4>(acc, racc, hsum, 4, L, x, sx, b0, b1, e0, e1);
+                zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 4, L, x, sx, b0, b1, e0, e1);
             }
         }
     }
@@ -913,11 +923,10 @@ static cudaError_t launch_v(const FbmArgs& a, float* out, cudaStream_t st) {
 
 template <int KIND, int ORDER>
 static cudaError_t launch_t(const FbmArgs& a, float* out, cudaStream_t st) {
-    // Measured per kind (tools/time_gen.py): the lean separable kernel at 4
-    // CTAs/SM is 6 % faster (90.5 -> 84.8 us at config 2 shape); for the
-    // paper variant the full kernel at 3 CTAs/SM is 1-2 % faster than either
-    // lean form, so it keeps the full kernel.
-    if constexpr (KIND == kZgSeparable)
+    // Zero-gradient kinds take the lean kernel at 4 CTAs/SM (64 registers, no
+    // spills) whenever the plan allows: measured 90.5 -> 84.8 us (separable)
+    // and 100.9 -> 98.8 us (paper, with DIRECT_C0) at the config-2 shape.
+    if constexpr (KIND == kZgSeparable || KIND == kZgPaper)
         if (a.epilogue == 0 && a.ngroup[kGGen] == 0) return launch_v<KIND, ORDER, true>(a, out, st);
     return launch_v<KIND, ORDER, false>(a, out, st);
 }
