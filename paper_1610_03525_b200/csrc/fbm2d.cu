@@ -283,6 +283,9 @@ __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRP
     }
 }
 
+#ifndef TG_COLS
+#define TG_COLS 1
+#endif
 #ifndef TG_ZG_LEAN_MIN_BLOCKS
 #define TG_ZG_LEAN_MIN_BLOCKS 4
 #endif
@@ -292,6 +295,47 @@ __device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRP
 #ifndef TG_HSUM
 #define TG_HSUM true
 #endif
+// Column form of the same cell (lean kernels): with the column features
+// e1 = dy + a*x (paper) / dy + a*Sx (separable) and e2 = a*(Sx - x),
+//   paper      v = (h00 + Sx*dx) + Sy*e1 + y*e2   -> 2 FFMA per pixel,
+//   separable  v = (h00 + Sx*dx) + Sy*e1          -> 1 FFMA per pixel,
+// the column-constant part accumulating in cacc[4] (4 registers instead of
+// the 8 row accumulators) and h00 in one per-thread sum when the cell covers
+// all the thread's rows (ONE_CELL); otherwise (ppc = 4, two cell rows) the
+// column constant of this cell row is added per pixel.  Per row only
+// (y, Sy) is loaded.
+template <int KIND, int NR, bool ONE_CELL>
+__device__ __forceinline__ void zg_cols(float (&acc)[kRPT][4], float (&cacc)[4], float& hsum, int r_begin,
+                                        const float4* __restrict__ Ly, const float (&x)[4],
+                                        const float (&sx)[4], const float (&smx)[4], float h00, float h10,
+                                        float h01, float h11) {
+    const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+    if constexpr (ONE_CELL) hsum += h00;
+    float e0[4], e1[4], e2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if constexpr (ONE_CELL) cacc[j] = fmaf(sx[j], dx, cacc[j]);
+        else e0[j] = fmaf(sx[j], dx, h00);
+        if constexpr (KIND == kZgPaper) {
+            e1[j] = fmaf(a, x[j], dy);
+            e2[j] = a * smx[j];
+        } else {
+            e1[j] = fmaf(a, sx[j], dy);
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+        const int r = r_begin + rr;
+        const float4 f = Ly[rr];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float base = ONE_CELL ? acc[r][j] : acc[r][j] + e0[j];
+            if constexpr (KIND == kZgPaper) acc[r][j] = fmaf(f.x, e2[j], fmaf(f.y, e1[j], base));
+            else acc[r][j] = fmaf(f.y, e1[j], base);
+        }
+    }
+}
+
 #ifndef TG_ZG_MIN_BLOCKS
 #define TG_ZG_MIN_BLOCKS 3
 #endif
@@ -455,6 +499,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     float acc[kRPT][4];
     float racc[kRPT];  // per-row terms common to the 4 columns (zg block modes)
     float hsum = 0.f;  // term common to all 32 pixels (zg block modes)
+    float cacc[4] = {0.f, 0.f, 0.f, 0.f};  // per-column terms (lean zg block modes)
 #pragma unroll
     for (int r = 0; r < kRPT; ++r) {
         racc[r] = 0.f;
@@ -472,15 +517,20 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const int yo = static_cast<int>(ty0 & mask) + r0;
             const float* g = grid + od.goff + (yo >> sh) * od.pitch + (xo >> sh);
             const float amp = od.amp * 0x1p-63f;
-            float x[4], sx[4];
+            float x[4], sx[4], smx[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float4 e = L[(xo & mask) + j];
                 x[j] = e.x;
                 sx[j] = e.y;
+                smx[j] = e.z;
             }
-            zg_rows<KIND, kRPT, TG_HSUM, LEAN>(acc, racc, hsum, 0, L + (yo & mask), x, sx, amp * g[0], amp * g[1], amp * g[od.pitch],
-                             amp * g[od.pitch + 1]);
+            if constexpr (LEAN && TG_COLS)
+                zg_cols<KIND, kRPT, true>(acc, cacc, hsum, 0, L + (yo & mask), x, sx, smx, amp * g[0], amp * g[1],
+                                          amp * g[od.pitch], amp * g[od.pitch + 1]);
+            else
+                zg_rows<KIND, kRPT, TG_HSUM, LEAN>(acc, racc, hsum, 0, L + (yo & mask), x, sx, amp * g[0],
+                                                   amp * g[1], amp * g[od.pitch], amp * g[od.pitch + 1]);
         }
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
         for (int q = 0; q < args.ngroup[kGBlk4]; ++q) {
@@ -489,18 +539,23 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const int pitch = od.pitch;
             const float* g = grid + od.goff + (r0 >> 2) * pitch + (c0 >> 2);
             const float amp = od.amp * 0x1p-63f;
-            float x[4], sx[4];
+            float x[4], sx[4], smx[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float4 e = L[j];
                 x[j] = e.x;
                 sx[j] = e.y;
+                smx[j] = e.z;
             }
             const float a0 = amp * g[0], a1 = amp * g[1];
             const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
-            zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 0, L, x, sx, a0, a1, b0, b1);
-            if constexpr (kRPT == 8) {
-                const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
+            static_assert(kRPT == 8, "ppc-4 blocks assume 8 rows per thread (two cell rows)");
+            const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
+            if constexpr (LEAN && TG_COLS) {
+                zg_cols<KIND, 4, false>(acc, cacc, hsum, 0, L, x, sx, smx, a0, a1, b0, b1);
+                zg_cols<KIND, 4, false>(acc, cacc, hsum, 4, L, x, sx, smx, b0, b1, e0, e1);
+            } else {
+                zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 0, L, x, sx, a0, a1, b0, b1);
                 zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 4, L, x, sx, b0, b1, e0, e1);
             }
         }
@@ -511,7 +566,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] += racc[r] + hsum;
+            for (int j = 0; j < 4; ++j) acc[r][j] += (racc[r] + hsum) + cacc[j];
             racc[r] = 0.f;
         }
     }
