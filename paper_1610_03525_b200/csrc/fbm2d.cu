@@ -247,55 +247,7 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch
 
 // zero-gradient cell rows r_begin.. of one cell: c0 = h00 + sy*dy goes into
 // the per-row accumulator (common to the 4 columns), the rest per pixel.
-// DIRECT_C0 (lean paper kernel): the column-independent term is added per
-// pixel instead of through the row accumulators, whose 8 registers the
-// 4-CTA/SM (64-register) lean kernel cannot afford.
-template <int KIND, int NR, bool ONE_CELL = false, bool DIRECT_C0 = false>
-__device__ __forceinline__ void zg_rows(float (&acc)[kRPT][4], float (&racc)[kRPT], float& hsum, int r_begin,
-                                        const float4* __restrict__ Ly, const float (&x)[4],
-                                        const float (&sx)[4], float h00, float h10, float h01,
-                                        float h11) {
-    const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
-    // ONE_CELL: h00 is common to every pixel of the thread -> one add per octave
-    if constexpr (ONE_CELL) hsum += h00;
-#pragma unroll
-    for (int rr = 0; rr < NR; ++rr) {
-        const int r = r_begin + rr;
-        const float4 f = Ly[rr];
-        if constexpr (DIRECT_C0 && KIND == kZgPaper) {
-            const float c0 = ONE_CELL ? f.y * dy : fmaf(f.y, dy, h00);
-            const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j] + c0));
-            continue;
-        }
-        if constexpr (ONE_CELL) racc[r] = fmaf(f.y, dy, racc[r]);
-        else racc[r] += fmaf(f.y, dy, h00);
-        if constexpr (KIND == kZgPaper) {
-            const float c1 = fmaf(a, f.x, dx), c2 = a * f.z;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(x[j], c2, fmaf(sx[j], c1, acc[r][j]));
-        } else {
-            const float c1 = fmaf(a, f.y, dx);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(sx[j], c1, acc[r][j]);
-        }
-    }
-}
-
-#ifndef TG_COLS
-#define TG_COLS 1
-#endif
-#ifndef TG_ZG_LEAN_MIN_BLOCKS
-#define TG_ZG_LEAN_MIN_BLOCKS 4
-#endif
-#ifndef TG_TMA_STORE
-#define TG_TMA_STORE 1
-#endif
-#ifndef TG_HSUM
-#define TG_HSUM true
-#endif
-// Column form of the same cell (lean kernels): with the column features
+// Zero-gradient cell in column form: with the column features
 // e1 = dy + a*x (paper) / dy + a*Sx (separable) and e2 = a*(Sx - x),
 //   paper      v = (h00 + Sx*dx) + Sy*e1 + y*e2   -> 2 FFMA per pixel,
 //   separable  v = (h00 + Sx*dx) + Sy*e1          -> 1 FFMA per pixel,
@@ -338,6 +290,12 @@ __device__ __forceinline__ void zg_cols(float (&acc)[kRPT][4], float (&cacc)[4],
 
 #ifndef TG_ZG_MIN_BLOCKS
 #define TG_ZG_MIN_BLOCKS 3
+#endif
+#ifndef TG_ZG_LEAN_MIN_BLOCKS
+#define TG_ZG_LEAN_MIN_BLOCKS 4
+#endif
+#ifndef TG_TMA_STORE
+#define TG_TMA_STORE 1
 #endif
 #ifndef TG_GEN_MIN_BLOCKS
 #define TG_GEN_MIN_BLOCKS 1
@@ -497,9 +455,9 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 
     // ---- evaluation of the thread's 4 x 8 pixels (no barriers) --------------
     float acc[kRPT][4];
-    float racc[kRPT];  // per-row terms common to the 4 columns (zg block modes)
+    float racc[kRPT];  // per-row terms common to the 4 columns (Perlin/generic block modes)
     float hsum = 0.f;  // term common to all 32 pixels (zg block modes)
-    float cacc[4] = {0.f, 0.f, 0.f, 0.f};  // per-column terms (lean zg block modes)
+    float cacc[4] = {0.f, 0.f, 0.f, 0.f};  // per-column terms (zg block modes)
 #pragma unroll
     for (int r = 0; r < kRPT; ++r) {
         racc[r] = 0.f;
@@ -525,12 +483,8 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                 sx[j] = e.y;
                 smx[j] = e.z;
             }
-            if constexpr (LEAN && TG_COLS)
-                zg_cols<KIND, kRPT, true>(acc, cacc, hsum, 0, L + (yo & mask), x, sx, smx, amp * g[0], amp * g[1],
-                                          amp * g[od.pitch], amp * g[od.pitch + 1]);
-            else
-                zg_rows<KIND, kRPT, TG_HSUM, LEAN>(acc, racc, hsum, 0, L + (yo & mask), x, sx, amp * g[0],
-                                                   amp * g[1], amp * g[od.pitch], amp * g[od.pitch + 1]);
+            zg_cols<KIND, kRPT, true>(acc, cacc, hsum, 0, L + (yo & mask), x, sx, smx, amp * g[0], amp * g[1],
+                                      amp * g[od.pitch], amp * g[od.pitch + 1]);
         }
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
         for (int q = 0; q < args.ngroup[kGBlk4]; ++q) {
@@ -551,24 +505,17 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
             static_assert(kRPT == 8, "ppc-4 blocks assume 8 rows per thread (two cell rows)");
             const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
-            if constexpr (LEAN && TG_COLS) {
-                zg_cols<KIND, 4, false>(acc, cacc, hsum, 0, L, x, sx, smx, a0, a1, b0, b1);
-                zg_cols<KIND, 4, false>(acc, cacc, hsum, 4, L, x, sx, smx, b0, b1, e0, e1);
-            } else {
-                zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 0, L, x, sx, a0, a1, b0, b1);
-                zg_rows<KIND, 4, false, LEAN>(acc, racc, hsum, 4, L, x, sx, b0, b1, e0, e1);
-            }
+            zg_cols<KIND, 4, false>(acc, cacc, hsum, 0, L, x, sx, smx, a0, a1, b0, b1);
+            zg_cols<KIND, 4, false>(acc, cacc, hsum, 4, L, x, sx, smx, b0, b1, e0, e1);
         }
     }
     if constexpr (kZg) {
-        // the row terms are complete: fold them in so racc is dead from here
-        // on (frees 8 registers for the hashing phases: fewer spills, -6 %)
+        // the column and per-thread terms are complete: fold them in so those
+        // registers are free for the hashing phases
 #pragma unroll
-        for (int r = 0; r < kRPT; ++r) {
+        for (int r = 0; r < kRPT; ++r)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] += (racc[r] + hsum) + cacc[j];
-            racc[r] = 0.f;
-        }
+            for (int j = 0; j < 4; ++j) acc[r][j] += hsum + cacc[j];
     }
 
     // ppc == 2: columns (0,1) | (2,3) are two cells at x = 0.25, 0.75; rows
@@ -978,9 +925,9 @@ static cudaError_t launch_v(const FbmArgs& a, float* out, cudaStream_t st) {
 
 template <int KIND, int ORDER>
 static cudaError_t launch_t(const FbmArgs& a, float* out, cudaStream_t st) {
-    // Zero-gradient kinds take the lean kernel at 4 CTAs/SM (64 registers, no
-    // spills) whenever the plan allows: measured 90.5 -> 84.8 us (separable)
-    // and 100.9 -> 98.8 us (paper, with DIRECT_C0) at the config-2 shape.
+    // Zero-gradient kinds take the lean kernel at 4 CTAs/SM (64 registers)
+    // whenever the plan allows: measured 90.5 -> 84.0 us (separable) and
+    // 100.9 -> 94.5 us (paper) at the config-2 shape.
     if constexpr (KIND == kZgSeparable || KIND == kZgPaper)
         if (a.epilogue == 0 && a.ngroup[kGGen] == 0) return launch_v<KIND, ORDER, true>(a, out, st);
     return launch_v<KIND, ORDER, false>(a, out, st);
