@@ -831,7 +831,11 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
         float* stage = grid;
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
-            float w[4] = {acc[r][0] + racc[r], acc[r][1] + racc[r], acc[r][2] + racc[r], acc[r][3] + racc[r]};
+            const float rr_ = kZg ? 0.f : racc[r];  // zg never uses the row accumulators
+            float w[4] = {acc[r][0], acc[r][1], acc[r][2], acc[r][3]};
+            if constexpr (!kZg)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) w[j] += rr_;
             if (!LEAN && args.epilogue) {
                 const float invR = static_cast<float>(1.0 / args.R);
                 const float vv = (static_cast<float>(ty0 + r0 + r) + 0.5f) * invR;
@@ -869,8 +873,13 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     for (int r = 0; r < kRPT; ++r, row += args.ld) {
         const int64_t ly = ly0 + r;
         if (ly < 0 || ly >= args.height) continue;
-        float v0 = acc[r][0] + racc[r], v1 = acc[r][1] + racc[r];
-        float v2 = acc[r][2] + racc[r], v3 = acc[r][3] + racc[r];
+        float v0 = acc[r][0], v1 = acc[r][1], v2 = acc[r][2], v3 = acc[r][3];
+        if constexpr (!kZg) {  // zg never uses the row accumulators
+            v0 += racc[r];
+            v1 += racc[r];
+            v2 += racc[r];
+            v3 += racc[r];
+        }
         if (!LEAN && args.epilogue) {
             // texture::render (texture.hpp:57-68) fused into the store:
             // sin(2 pi f phase + gain * noise), (u, v) pixel centres in [0, 1)
