@@ -27,6 +27,10 @@ namespace tg {
 
 namespace {
 
+#ifndef TG_3D_LEAN_MIN_BLOCKS
+#define TG_3D_LEAN_MIN_BLOCKS 4
+#endif
+
 constexpr int kThreads3 = 256;
 constexpr int kTX = 128, kTY = 8, kTZ = 8;
 constexpr int kCap3 = 13312;  // corner floats per CTA
@@ -88,14 +92,24 @@ struct Smem3 {
     float grid[kCap3];
 };
 
+// Lean kernels (no general octaves) use only the corner grid: 53 KB, so 4
+// CTAs fit an SM.
+template <bool LEAN>
+constexpr size_t smem3() {
+    return LEAN ? sizeof(float) * kCap3 : sizeof(Smem3);
+}
+
 // LEAN: no general octaves in the plan (host-decided): the per-voxel general
 // path is compiled out, which lowers the register pressure of the rest
-// enough for 3 CTAs per SM (80 registers; 0.96 -> 0.87 ms at config 4).
+// enough for 4 CTAs per SM (64 registers, no spills; with the 53 KB
+// corner-only shared memory: 0.96 -> 0.87 (3 CTAs) -> 0.81 ms at config 4).
 template <int ORDER, bool LEAN>
-__global__ void __launch_bounds__(kThreads3, LEAN ? 3 : 2)
+__global__ void __launch_bounds__(kThreads3, LEAN ? TG_3D_LEAN_MIN_BLOCKS : 2)
 fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char raw3[];
     Smem3& S = *reinterpret_cast<Smem3*>(raw3);
+    // lean kernels have no sampling tables: the corner grid starts at 0
+    float* const grid3 = LEAN ? reinterpret_cast<float*>(raw3) : S.grid;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tx0 = a.tile_x0 + static_cast<int64_t>(blockIdx.x) * kTX;
     const int64_t ty0 = a.tile_y0 + static_cast<int64_t>(blockIdx.y) * kTY;
@@ -126,6 +140,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
             coord3(od, a.R, tz0, &iz0, &t);
             coord3(od, a.R, tz0 + kTZ - 1, &e, &t);
             ncz = static_cast<int>(e - iz0 + 2);
+            if constexpr (LEAN) __trap();  // the host never sends general octaves to a lean kernel
             Tab3& tb = S.tab[od.tslot];
             if (tid < kTX) {
                 int64_t i;
@@ -154,7 +169,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         }
         const uint64_t p0 = pack3(base, ix0, iy0, iz0);
         const int pitch = od.pitch, plane = pitch * od.ncy;  // strides use the planned bounds
-        float* g = S.grid + od.goff;
+        float* g = grid3 + od.goff;
         const int nrows = ncy * ncz;
         if (od.lut_off >= 0 && od.shift == 0) {
             // ppc = 1: 129 x 9 x 9 corners; 4 consecutive x per lane (four hash
@@ -233,7 +248,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         }
 
         if (mode == kM3P1) {  // x = y = z = 1/2: the mean of the 8 corners
-            const float* g = S.grid + od.goff + warp * pitch + c0;
+            const float* g = grid3 + od.goff + warp * pitch + c0;
             const float q = 0.125f * amp;
             auto face = [&](int z, float (&F)[4]) {
                 const float* r0p = g + z * plane;
@@ -272,7 +287,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
             float sx[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) sx[j] = L[(xo + j) & mask].y;
-            const float* gy = S.grid + od.goff + (yo >> sh) * pitch;
+            const float* gy = grid3 + od.goff + (yo >> sh) * pitch;
             if (sh >= 2) {
                 // the thread's 4 columns share one x-cell; B0 -> per-slice accumulator
                 const float* g = gy + (xo >> sh);
@@ -368,7 +383,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 float h[8];
                 if (!direct) {
                     const int b = static_cast<int>(iz) * plane + static_cast<int>(iy) * pitch + static_cast<int>(ixj[j]);
-                    const float* q = S.grid + od.goff + b;
+                    const float* q = grid3 + od.goff + b;
                     h[0] = q[0];
                     h[1] = q[1];
                     h[2] = q[pitch];
@@ -409,14 +424,14 @@ cudaError_t launch3v(const Fbm3Args& a, float* out, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(fbm3d_kernel<ORDER, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(sizeof(Smem3)));
+                                             static_cast<int>(smem3<LEAN>()));
         if (e != cudaSuccess) return e;
         configured = true;
     }
     dim3 grid(static_cast<unsigned>((a.ox + a.nx - a.tile_x0 + kTX - 1) / kTX),
               static_cast<unsigned>((a.oy + a.ny - a.tile_y0 + kTY - 1) / kTY),
               static_cast<unsigned>((a.oz + a.nz - a.tile_z0 + kTZ - 1) / kTZ));
-    fbm3d_kernel<ORDER, LEAN><<<grid, kThreads3, sizeof(Smem3), st>>>(a, out);
+    fbm3d_kernel<ORDER, LEAN><<<grid, kThreads3, smem3<LEAN>(), st>>>(a, out);
     return cudaGetLastError();
 }
 
