@@ -459,13 +459,75 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     float hsum = 0.f;  // term common to all 32 pixels (zg block modes)
     float cacc[4] = {0.f, 0.f, 0.f, 0.f};  // per-column terms (zg block modes)
 #pragma unroll
-    for (int r = 0; r < kRPT; ++r) {
-        racc[r] = 0.f;
+    for (int r = 0; r < kRPT; ++r) racc[r] = 0.f;
+
+    if constexpr (KIND == kZgPaper) {
+        // power-of-two ppc >= 8, all block octaves summed in separated form.
+        // With x = x0 + c/ppc, y = y0 + r/ppc (c = 0..3, r = 0..7 the pixel's
+        // place in the thread's block) the paper cell
+        //   v = h00 + Sx*dx + Sy*(dy + a*x) + y*a*(Sx - x)
+        // is  v = [h00 + Sx*dx + (a*y0)*(Sx - x)] + r*[(a/ppc)*(Sx - x)]
+        //       + Sy*(dy + a*x0) + c*[Sy*(a/ppc)]
+        // i.e. column terms C0(c), C1(c) and row terms R0(r), R1(r) that
+        // add up over octaves; the pixels are formed once after the list:
+        //   v(c, r) = C0(c) + R0(r) + c*R1(r) + r*C1(c).
+        float C0[4] = {0.f, 0.f, 0.f, 0.f}, C1[4] = {0.f, 0.f, 0.f, 0.f}, R0[kRPT], R1[kRPT];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
+        for (int r = 0; r < kRPT; ++r) R0[r] = R1[r] = 0.f;
+        const float* lutS = reinterpret_cast<const float*>(args.lut + kLutN4);  // S(x)
+        const float* lutD = lutS + kLutN4;                                       // S(x) - x
+        for (int q = 0; q < args.ngroup[kGBlk8]; ++q) {
+            const OctDev& od = args.oct[args.group[kGBlk8][q]];
+            const int sh = od.shift, mask = od.ppc - 1;
+            const int xo = static_cast<int>(tx0 & mask) + c0;
+            const int yo = static_cast<int>(ty0 & mask) + r0;
+            const int mx = xo & mask, my = yo & mask;  // multiples of 4 and 8
+            const float* g = grid + od.goff + (yo >> sh) * od.pitch + (xo >> sh);
+            const float amp = od.amp * 0x1p-63f;
+            const float h00 = amp * g[0], h10 = amp * g[1], h01 = amp * g[od.pitch], h11 = amp * g[od.pitch + 1];
+            const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+            const float inv = od.inv_ppc;  // exact power of two
+            const float x0 = (static_cast<float>(mx) + 0.5f) * inv, y0 = (static_cast<float>(my) + 0.5f) * inv;
+            const float4 sx = __ldg(reinterpret_cast<const float4*>(lutS + od.ppc + mx));
+            const float4 dd = __ldg(reinterpret_cast<const float4*>(lutD + od.ppc + mx));
+            const float sxa[4] = {sx.x, sx.y, sx.z, sx.w}, dda[4] = {dd.x, dd.y, dd.z, dd.w};
+            const float ay0 = a * y0, ad = a * inv, k0 = fmaf(a, x0, dy);
+            hsum += h00;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                C0[j] = fmaf(dda[j], ay0, fmaf(sxa[j], dx, C0[j]));
+                C1[j] = fmaf(dda[j], ad, C1[j]);
+            }
+#pragma unroll
+            for (int r4 = 0; r4 < kRPT; r4 += 4) {
+                const float4 sy = __ldg(reinterpret_cast<const float4*>(lutS + od.ppc + my + r4));
+                const float sya[4] = {sy.x, sy.y, sy.z, sy.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    R0[r4 + i] = fmaf(sya[i], k0, R0[r4 + i]);
+                    R1[r4 + i] = fmaf(sya[i], ad, R1[r4 + i]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kRPT; ++r) {
+            const float rr = R0[r] + hsum;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float v = C0[j] + rr;
+                if (r) v = fmaf(static_cast<float>(r), C1[j], v);
+                if (j) v = fmaf(static_cast<float>(j), R1[r], v);
+                acc[r][j] = v;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < kRPT; ++r)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
     }
 
-    if constexpr (kZg) {
+    if constexpr (KIND == kZgSeparable) {
         // power-of-two ppc >= 8: the 4 x 8 block lies in one cell
         for (int q = 0; q < args.ngroup[kGBlk8]; ++q) {
             const OctDev& od = args.oct[args.group[kGBlk8][q]];
@@ -486,6 +548,8 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             zg_cols<KIND, kRPT, true>(acc, cacc, hsum, 0, L + (yo & mask), x, sx, smx, amp * g[0], amp * g[1],
                                       amp * g[od.pitch], amp * g[od.pitch + 1]);
         }
+    }
+    if constexpr (kZg) {
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
         for (int q = 0; q < args.ngroup[kGBlk4]; ++q) {
             const OctDev& od = args.oct[args.group[kGBlk4][q]];
@@ -509,7 +573,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
             zg_cols<KIND, 4, false>(acc, cacc, hsum, 4, L, x, sx, smx, b0, b1, e0, e1);
         }
     }
-    if constexpr (kZg) {
+    if constexpr (KIND == kZgSeparable) {
         // the column and per-thread terms are complete: fold them in so those
         // registers are free for the hashing phases
 #pragma unroll

@@ -36,6 +36,7 @@ constexpr int kTileH = 8 * kRPT;   // 8 warps x kRPT rows
 constexpr int kGridCap = kRPT == 8 ? 12288 : 6656;  // lattice-corner floats per channel per CTA
 constexpr int kTabSlots = 4;       // per-CTA sampling tables (general octaves)
 constexpr int kLutLog2Max = 13;    // device row LUT covers ppc = 1 .. 8192
+constexpr int kLutN4 = 2 << kLutLog2Max;  // float4 entries before the planar S / S-x copies
 
 // Per-octave evaluation mode: a function of the configuration only (never of
 // the window), so every window reproduces the full-map bits.

@@ -48,7 +48,10 @@ cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uin
 
 // Row LUTs (kernels2d::build_row_lut at phase 0.5, kernels2d.hpp:214-239) for
 // every power-of-two ppc up to 2^kLutLog2Max, both smoothstep orders, computed
-// once per device in fp64 and rounded to fp32: entry (x, S(x), S(x)-x, x*S(x)).
+// once per device in fp64 and rounded to fp32: entry (x, S(x), S(x)-x, x*S(x))
+// at [ppc - 1 + r], followed by two planar copies, S(x) at float [ppc + r] and
+// S(x) - x at float [kLutN4 + ppc + r] past the kLutN4-entry float4 block, so
+// that 4 consecutive rows / columns are one aligned 16-byte load.
 // Immutable after creation, so concurrent callers share it (like the
 // reference's thread-local cached_row_lut, kernels2d.hpp:246-259).
 const float4* row_lut(int order) {
@@ -60,8 +63,8 @@ const float4* row_lut(int order) {
     const int oi = order == 5 ? 1 : 0;
     std::lock_guard<std::mutex> lock(mu);
     if (luts[dev][oi]) return luts[dev][oi];
-    const int n = (1 << (kLutLog2Max + 1)) - 1;
-    std::vector<float4> h(static_cast<size_t>(n));
+    std::vector<float4> h(static_cast<size_t>(kLutN4 + 2 * kLutN4 / 4), make_float4(0.f, 0.f, 0.f, 0.f));
+    float* planes = reinterpret_cast<float*>(h.data() + kLutN4);
     for (int k = 0; k <= kLutLog2Max; ++k) {
         const int ppc = 1 << k;
         for (int r = 0; r < ppc; ++r) {
@@ -69,11 +72,13 @@ const float4* row_lut(int order) {
             const double sv = order == 5 ? x * x * x * (10.0 + x * (6.0 * x - 15.0)) : x * x * (3.0 - 2.0 * x);
             h[static_cast<size_t>(ppc - 1 + r)] = make_float4(static_cast<float>(x), static_cast<float>(sv),
                                                               static_cast<float>(sv - x), static_cast<float>(x * sv));
+            planes[ppc + r] = static_cast<float>(sv);
+            planes[kLutN4 + ppc + r] = static_cast<float>(sv - x);
         }
     }
     float4* d = nullptr;
-    if (cudaMalloc(&d, sizeof(float4) * n) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, h.data(), sizeof(float4) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMalloc(&d, sizeof(float4) * h.size()) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h.data(), sizeof(float4) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaFree(d);
         return nullptr;
     }
