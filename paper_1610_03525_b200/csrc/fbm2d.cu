@@ -23,7 +23,11 @@
 //
 // Every pixel's arithmetic is a function of (config, global pixel) only, so
 // any window / tile decomposition reproduces the same bits (fbm.hpp:7-8).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+
+#include <mutex>
 
 #include "fbm_params.h"
 #include "lattice.cuh"
@@ -308,10 +312,11 @@ template <int KIND, int ORDER, bool LEAN>
 __global__ void __launch_bounds__(kThreads, (KIND == kZgPaper || KIND == kZgSeparable)
                                                 ? (LEAN ? TG_ZG_LEAN_MIN_BLOCKS : TG_ZG_MIN_BLOCKS)
                                                 : (KIND == kPerlin ? 2 : TG_GEN_MIN_BLOCKS))
-fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
+fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUtensorMap tmap,
+             float* __restrict__ out) {
     constexpr int CH = Traits<KIND>::kCh;
     constexpr bool kZg = KIND == kZgPaper || KIND == kZgSeparable;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     TabSlot* tabs = reinterpret_cast<TabSlot*>(smem_raw);
     float* grid = reinterpret_cast<float*>(smem_raw + (LEAN ? 0 : sizeof(TabSlot) * kTabSlots));
 
@@ -883,16 +888,17 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     const int64_t lx0 = tx0 + c0 - args.ox;
     const int64_t ly0 = ty0 + r0 - args.oy;
 #if TG_TMA_STORE
-    // Interior tiles: stage the 128 x 64 tile in shared memory (the corner
-    // grids are dead by now) and let the bulk-copy engine write each 512-byte
-    // row to HBM (cp.async.bulk, one lane per warp for the warp's 8 rows).
-    const bool tile_full = tx0 - args.ox >= 0 && tx0 - args.ox + kTW <= args.width && ty0 - args.oy >= 0 &&
-                           ty0 - args.oy + kTH <= args.height && ((tx0 - args.ox) & 3) == 0 &&
-                           (args.ld & 3) == 0 && (args.map_stride & 3) == 0 &&
-                           (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    if (tile_full) {  // uniform per CTA
-        __syncthreads();  // every warp is done reading the corner grids
-        float* stage = grid;
+    // Every tile (right / bottom edge tiles included: the tensor copy clips
+    // rows and columns outside the window) is staged in shared memory (the corner grids are
+    // dead by now) and written by the TMA engine, one 128 x 8 box per warp
+    // (cp.async.bulk.tensor, SASS UTMASTG) from the host-encoded tensor map of
+    // the output window.
+    // Box start coordinates must be non-negative (negative ones fault), so a
+    // warp whose rows start left of / above the window stores directly.
+    const bool tma_warp = args.tma && tx0 >= args.ox && ty0 + r0 >= args.oy;
+    if (args.tma) __syncthreads();  // uniform per launch: every warp is done reading the corner grids
+    if (tma_warp) {
+        float* stage = grid + r0 * kTW;
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
             const float rr_ = kZg ? 0.f : racc[r];  // zg never uses the row accumulators
@@ -911,18 +917,18 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
                     w[j] = sinf(fmaf(args.tex_freq2pi, phase, args.tex_gain * w[j]));
                 }
             }
-            *reinterpret_cast<float4*>(stage + (r0 + r) * kTW + c0) = make_float4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<float4*>(stage + r * kTW + c0) = make_float4(w[0], w[1], w[2], w[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-            float* grow = out + static_cast<int64_t>(blockIdx.z) * args.map_stride + ly0 * args.ld + (tx0 - args.ox);
-            const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(stage + r0 * kTW));
-#pragma unroll
-            for (int r = 0; r < kRPT; ++r)
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(grow + r * args.ld),
-                             "r"(s0 + r * kTW * 4), "n"(kTW * 4)
-                             : "memory");
+            const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmap)),
+                "r"(static_cast<int32_t>(tx0 - args.ox)), "r"(static_cast<int32_t>(ty0 + r0 - args.oy)),
+                "r"(static_cast<int32_t>(blockIdx.z)), "r"(sa)
+                : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
@@ -976,8 +982,38 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
 
 // ---- launch ------------------------------------------------------------------
 
+// Tensor map of the output window for the TMA tile store: dims (width,
+// height, maps), fp32, box 128 x 8 x 1 (one warp's rows).  Needs a 16-byte
+// aligned base and row / map strides that are multiples of 16 bytes; the
+// caller falls back to vector stores otherwise.
+static bool encode_out_map(const FbmArgs& a, float* out, CUtensorMap* m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!encode) return false;
+    if ((reinterpret_cast<uintptr_t>(out) & 15) || (a.ld & 3) || a.width < 1 || a.height < 1 ||
+        a.width > (int64_t(1) << 31) || a.height > (int64_t(1) << 31) || a.ld < a.width)
+        return false;
+    const int64_t mstride = a.n_maps > 1 ? a.map_stride : a.ld * a.height;
+    if ((mstride & 3) || mstride < a.ld * a.height) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.width), static_cast<cuuint64_t>(a.height),
+                                static_cast<cuuint64_t>(a.n_maps)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.ld) * 4, static_cast<cuuint64_t>(mstride) * 4};
+    const cuuint32_t box[3] = {kTW, kRPT, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int KIND, int ORDER, bool LEAN>
-static cudaError_t launch_v(const FbmArgs& a, float* out, cudaStream_t st) {
+static cudaError_t launch_v(const FbmArgs& a0, float* out, cudaStream_t st) {
     constexpr size_t smem = smem_bytes<KIND, LEAN>();
     auto kern = fbm2d_kernel<KIND, ORDER, LEAN>;
     static bool configured = false;  // benign race: idempotent attribute set
@@ -987,12 +1023,16 @@ static cudaError_t launch_v(const FbmArgs& a, float* out, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    FbmArgs a = a0;
+    CUtensorMap m;
+    a.tma = TG_TMA_STORE && encode_out_map(a, out, &m) ? 1 : 0;
+    if (!a.tma) memset(&m, 0, sizeof(m));
     constexpr int TH = kTH;
     const int64_t tiles_x = (a.ox + a.width - a.tile_x0 + kTW - 1) / kTW;
     const int64_t tiles_y = (a.oy + a.height - a.tile_y0 + TH - 1) / TH;
     dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
               static_cast<unsigned>(a.n_maps));
-    kern<<<grid, kThreads, smem, st>>>(a, out);
+    kern<<<grid, kThreads, smem, st>>>(a, m, out);
     return cudaGetLastError();
 }
 
