@@ -53,19 +53,19 @@ template <> struct Traits<kGeneric> { static constexpr int kCh = 3; };
 // Corner data of one lattice point from its packed key (lattice.hpp:46-50),
 // scaled like the reference's render paths: zg/generic heights x amp
 // (fbm.hpp:270,349), Perlin unit gradients x amp (409-420), generic gradients
-// x w, unscaled by amp (348).  amp63 = amp * 2^-63 (height_scaled_from_pre).
+// x w, unscaled by amp (348).  amp63 = amp * kMapScale (map_height).
 // ZeroSource (fbm.hpp:125-133) is amp = w = 0, set by the host planner.
 template <int KIND>
 __device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float amp63, float w, float* d) {
     if constexpr (KIND == kZgPaper || KIND == kZgSeparable) {
-        d[0] = amp63 * height_scaled(p);
+        d[0] = amp63 * map_height(p);
     } else if constexpr (KIND == kPerlin) {
         float c, s;
         fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
         d[0] = amp * c;
         d[1] = amp * s;
     } else {
-        d[0] = amp63 * height_scaled(p);
+        d[0] = amp63 * map_height(p);
         float c, s;
         fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
         const float m = unit_from_hash(mix64(p ^ kMagnitudeLane)) * w;
@@ -77,7 +77,7 @@ __device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float 
 template <int KIND>
 __device__ __forceinline__ void corner_data(uint64_t base, int64_t ix, int64_t iy, float amp, float w,
                                             float* d) {
-    corner_data_packed<KIND>(pack_xy(base, ix, iy), amp, amp * 0x1p-63f, w, d);
+    corner_data_packed<KIND>(pack_xy(base, ix, iy), amp, amp * kMapScale, w, d);
 }
 
 // Per-cell constants (from the 4 corners) and per-(cell,row) coefficients.
@@ -329,12 +329,12 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     const int c0 = lane * 4;
     const int r0 = warp * kRPT;
 
-    // Grid contents: zero-gradient grids hold raw height_scaled() values (the
+    // Grid contents: zero-gradient grids hold raw map_height() values (the
     // octave amplitude is folded in at evaluation); Perlin/generic grids hold
     // amplitude-scaled corner data.
     auto grid_value = [&](uint64_t p, const OctDev& od, float* d) {
-        if constexpr (kZg) d[0] = height_scaled(p);
-        else corner_data_packed<KIND>(p, od.amp, od.amp * 0x1p-63f, od.w, d);
+        if constexpr (kZg) d[0] = map_height(p);
+        else corner_data_packed<KIND>(p, od.amp, od.amp * kMapScale, od.w, d);
     };
 
     // ---- prologue: every octave's tile corners (and, for general octaves,
@@ -408,7 +408,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
                 if constexpr (kZg) {
                     float h[4];
-                    height_scaled4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
+                    map_height4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
                     *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
                 } else {
                     float d[4][CH];
@@ -488,7 +488,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const int yo = static_cast<int>(ty0 & mask) + r0;
             const int mx = xo & mask, my = yo & mask;  // multiples of 4 and 8
             const float* g = grid + od.goff + (yo >> sh) * od.pitch + (xo >> sh);
-            const float amp = od.amp * 0x1p-63f;
+            const float amp = od.amp * kMapScale;
             const float h00 = amp * g[0], h10 = amp * g[1], h01 = amp * g[od.pitch], h11 = amp * g[od.pitch + 1];
             const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
             const float inv = od.inv_ppc;  // exact power of two
@@ -541,7 +541,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const int xo = static_cast<int>(tx0 & mask) + c0;
             const int yo = static_cast<int>(ty0 & mask) + r0;
             const float* g = grid + od.goff + (yo >> sh) * od.pitch + (xo >> sh);
-            const float amp = od.amp * 0x1p-63f;
+            const float amp = od.amp * kMapScale;
             float x[4], sx[4], smx[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -561,7 +561,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const float4* L = args.lut + od.lut_off;  // 4 entries: x = 1/8, 3/8, 5/8, 7/8
             const int pitch = od.pitch;
             const float* g = grid + od.goff + (r0 >> 2) * pitch + (c0 >> 2);
-            const float amp = od.amp * 0x1p-63f;
+            const float amp = od.amp * kMapScale;
             float x[4], sx[4], smx[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -593,7 +593,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const OctDev& od = args.oct[args.group[kGBlk2][q]];
         const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
         const int pitch = od.pitch;
-        const float sc = kZg ? od.amp * 0x1p-63f : 1.0f;
+        const float sc = kZg ? od.amp * kMapScale : 1.0f;
         const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
         float t[3][CH];
 #pragma unroll
@@ -635,7 +635,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const float* g = grid + od.goff + r0 * pitch + c0;
         if constexpr (kZg) {
             // every zero-gradient kernel is the mean of its 4 corners
-            ppc1_block(acc, 0.25f * (od.amp * 0x1p-63f), [&](int r, float (&h)[5]) {
+            ppc1_block(acc, 0.25f * (od.amp * kMapScale), [&](int r, float (&h)[5]) {
                 const float4 v = *reinterpret_cast<const float4*>(g + r * pitch);
                 h[0] = v.x;
                 h[1] = v.y;
@@ -682,7 +682,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     if constexpr (KIND != kPerlin) {
         for (int q = 0; q < args.ngroup[kGSub]; ++q) {
             const OctDev& od = args.oct[args.group[kGSub][q]];
-            const float amp = od.amp * 0x1p-63f;  // exact power-of-two rescale
+            const float amp = od.amp * kMapScale;  // exact power-of-two rescale
             const int64_t k = od.k, half = od.k >> 1;
             uint64_t X[4];
 #pragma unroll
@@ -692,7 +692,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
 #pragma unroll
             for (int r = 0; r < kRPT; ++r) {
                 float h[4];
-                height_scaled4(add64(X[0], Y), add64(X[1], Y), add64(X[2], Y), add64(X[3], Y), h);
+                map_height4(add64(X[0], Y), add64(X[1], Y), add64(X[2], Y), add64(X[3], Y), h);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, h[j], acc[r][j]);
                 Y = add64(Y, dY);
@@ -706,7 +706,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const int mode = od.mode;
         const uint64_t base = seed_key + od.oct_key;
         // grids of zg octaves hold raw heights: scale at load
-        const float gscale = kZg ? od.amp * 0x1p-63f : 1.0f;
+        const float gscale = kZg ? od.amp * kMapScale : 1.0f;
 
         if (mode == kModeBlock) {
             // Perlin/generic, power-of-two ppc >= 4: 4 columns share one cell

@@ -116,7 +116,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     const int64_t tz0 = a.tile_z0 + static_cast<int64_t>(blockIdx.z) * kTZ;
     const int c0 = lane * 4;
 
-    // ---- prologue: all octaves' tile corners (raw height_scaled values) ------
+    // ---- prologue: all octaves' tile corners (raw map_height values) ------
     for (int o = 0; o < a.octaves; ++o) {
         const OctDev& od = a.oct[o];
         const int mode = od.mode;
@@ -179,16 +179,16 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 const int cz = rw / ncy, cy = rw - cz * ncy;
                 const uint64_t p = px + static_cast<uint64_t>(cy) * kIyMul + static_cast<uint64_t>(cz) * kIzMul;
                 float4 v;
-                v.x = height_scaled(p);
-                v.y = height_scaled(add64(p, kIxMul));
-                v.z = height_scaled(add64(p, 2 * kIxMul));
-                v.w = height_scaled(add64(p, 3 * kIxMul));
+                v.x = map_height(p);
+                v.y = map_height(add64(p, kIxMul));
+                v.z = map_height(add64(p, 2 * kIxMul));
+                v.w = map_height(add64(p, 3 * kIxMul));
                 *reinterpret_cast<float4*>(g + cz * plane + cy * pitch + 4 * lane) = v;
             }
             for (int rw = tid; rw < nrows; rw += kThreads3) {
                 const int cz = rw / ncy, cy = rw - cz * ncy;
                 g[cz * plane + cy * pitch + kTX] =
-                    height_scaled(p0 + static_cast<uint64_t>(kTX) * kIxMul + static_cast<uint64_t>(cy) * kIyMul +
+                    map_height(p0 + static_cast<uint64_t>(kTX) * kIxMul + static_cast<uint64_t>(cy) * kIyMul +
                                   static_cast<uint64_t>(cz) * kIzMul);
             }
         } else {
@@ -205,7 +205,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                     const int cz = static_cast<int>((static_cast<float>(rw) + 0.5f) * ry);
                     const int cy = rw - cz * ncy;
                     dst[u] = cz * plane + cy * pitch + cx;
-                    d[u] = height_scaled(pack3(p0, cx, cy, cz));
+                    d[u] = map_height(pack3(p0, cx, cy, cz));
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -226,7 +226,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     for (int o = 0; o < a.octaves; ++o) {
         const OctDev& od = a.oct[o];
         const int mode = od.mode;
-        const float amp = od.amp * 0x1p-63f;
+        const float amp = od.amp * kMapScale;
         const uint64_t base = a.seed_key + od.oct_key;
         const int pitch = od.pitch, plane = od.pitch * od.ncy;
 
@@ -241,7 +241,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
 #pragma unroll
             for (int z = 0; z < kTZ; ++z) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(amp, height_scaled(add64(X[j], Z)), acc[z][j]);
+                for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(amp, map_height(add64(X[j], Z)), acc[z][j]);
                 Z = add64(Z, dZ);
             }
             continue;
@@ -395,7 +395,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 } else {
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
-                        h[k] = height_scaled(pack3(base, ixj[j] + (k & 1), iy + ((k >> 1) & 1), iz + ((k >> 2) & 1)));
+                        h[k] = map_height(pack3(base, ixj[j] + (k & 1), iy + ((k >> 1) & 1), iz + ((k >> 2) & 1)));
                 }
                 const float b0 = lerp(lerp(h[0], h[2], sy), lerp(h[4], h[6], sy), sz);
                 const float b1 = lerp(lerp(h[1], h[3], sy), lerp(h[5], h[7], sy), sz);

@@ -114,6 +114,70 @@ __device__ __forceinline__ float height_scaled(uint64_t packed) {
     return height_scaled_from_pre(lo, hi);
 }
 
+// Map-path corner height from the top word of fmix64 only.  The final
+// xorshift (z ^= z >> 33) touches only the low word, and the second multiply
+// needs only its high word (mul.hi of the low words plus both cross terms),
+// with the sign flip (z ^ 2^63 = z + 2^63) folded into its addend; one
+// s32 -> f32 conversion then gives RN(floor(corner_height * 2^31)), i.e. the
+// height to |error| <= 2^-31 + half an fp32 ulp (heights are checked within
+// the north star's 1e-5 tolerance; the hash itself and tg_lattice_height_f32
+// stay bit-exact).  11 instructions per key against 14 for height_scaled.
+__device__ __forceinline__ float height_hi(uint64_t p) {
+    uint32_t lo = static_cast<uint32_t>(p), hi = static_cast<uint32_t>(p >> 32);
+    lo ^= hi >> 1;
+    TG_MUL64(lo, hi, 0xED558CCD, 0xFF51AFD7);
+    lo ^= hi >> 1;
+    int32_t t;
+    asm("{\n\t.reg .b32 q;\n\tmad.hi.u32 q, %1, 0x1A85EC53, 0x80000000;\n\t"
+        "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
+        : "=r"(t)
+        : "r"(lo), "r"(hi));
+    return static_cast<float>(t);
+}
+
+// Four independent keys in lock step (see height_scaled4).
+__device__ __forceinline__ void height_hi4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&out)[4]) {
+    uint32_t l[4] = {static_cast<uint32_t>(p0), static_cast<uint32_t>(p1), static_cast<uint32_t>(p2),
+                     static_cast<uint32_t>(p3)};
+    uint32_t h[4] = {static_cast<uint32_t>(p0 >> 32), static_cast<uint32_t>(p1 >> 32),
+                     static_cast<uint32_t>(p2 >> 32), static_cast<uint32_t>(p3 >> 32)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) TG_MUL64(l[i], h[i], 0xED558CCD, 0xFF51AFD7);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int32_t t;
+        asm("{\n\t.reg .b32 q;\n\tmad.hi.u32 q, %1, 0x1A85EC53, 0x80000000;\n\t"
+            "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
+            : "=r"(t)
+            : "r"(l[i]), "r"(h[i]));
+        out[i] = static_cast<float>(t);
+    }
+}
+
+// The height representation of the map kernels: map_height(p) * kMapScale
+// is the corner height.  TG_MAP_HEIGHT_HI=0 selects the exactly rounded
+// height_scaled path (for A/B checks).
+#ifndef TG_MAP_HEIGHT_HI
+#define TG_MAP_HEIGHT_HI 1
+#endif
+#if TG_MAP_HEIGHT_HI
+constexpr float kMapScale = 0x1p-31f;
+__device__ __forceinline__ float map_height(uint64_t p) { return height_hi(p); }
+__device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
+    height_hi4(p0, p1, p2, p3, o);
+}
+#else
+constexpr float kMapScale = 0x1p-63f;
+__device__ __forceinline__ float map_height(uint64_t p) { return height_scaled(p); }
+__device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
+    height_scaled4(p0, p1, p2, p3, o);
+}
+#endif
+
 // float(corner_height) with one round-to-nearest (lattice.hpp:56-64).
 __device__ __forceinline__ float height_from_hash(uint64_t z) {
     const int64_t t = static_cast<int64_t>(z ^ 0x8000000000000000ULL) >> 11;
