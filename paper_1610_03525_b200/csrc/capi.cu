@@ -259,6 +259,15 @@ int device_ready() {
     return TG_OK;
 }
 
+// -sum of the octave amplitudes: the kernels' map_height values carry +1 per
+// corner height (lattice.cuh), and each cell blends its corners affinely, so
+// every octave's contribution is off by exactly +amp (removed once per pixel).
+static float amp_offset(const tg::OctDev* oct, int n) {
+    double s = 0.0;
+    for (int o = 0; o < n; ++o) s += static_cast<double>(oct[o].amp);
+    return static_cast<float>(-s);
+}
+
 int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, int64_t height,
                int64_t ld, tg::FbmArgs* a) {
     std::memset(a, 0, sizeof(*a));
@@ -279,6 +288,7 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     const int64_t cand[4] = {ox - 256, ox + width + 256, oy - 256, oy + height + 256};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
     plan_octaves(c, gmax, a->oct, true);
+    a->hoff = amp_offset(a->oct, c->octaves);
     // mode-homogeneous octave lists (fbm_params.h OctGroup)
     const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
     for (int o = 0; o < c->octaves; ++o) {
@@ -644,6 +654,7 @@ int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int6
     const int64_t cand[6] = {ox - 64, ox + nx + 64, oy - 64, oy + ny + 64, oz - 64, oz + nz + 64};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
     plan_octaves(cfg, gmax, a.oct, false);
+    a.hoff = amp_offset(a.oct, cfg->octaves);
     tg::fbm3d_plan(&a, 1);
     a.lut = tg::row_lut(order_of(cfg));
     if (!a.lut) return fail(TG_EDEVICE, "row LUT allocation failed");

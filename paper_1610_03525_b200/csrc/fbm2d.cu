@@ -461,7 +461,9 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     // ---- evaluation of the thread's 4 x 8 pixels (no barriers) --------------
     float acc[kRPT][4];
     float racc[kRPT];  // per-row terms common to the 4 columns (Perlin/generic block modes)
-    float hsum = 0.f;  // term common to all 32 pixels (zg block modes)
+    // term common to all 32 pixels (zg block modes), starting from the
+    // map_height offset of every octave (lattice.cuh)
+    float hsum = kMapOffset && KIND != kPerlin ? args.hoff : 0.f;
     float cacc[4] = {0.f, 0.f, 0.f, 0.f};  // per-column terms (zg block modes)
 #pragma unroll
     for (int r = 0; r < kRPT; ++r) racc[r] = 0.f;
@@ -526,10 +528,11 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             }
         }
     } else {
+        const float init = KIND == kGeneric ? hsum : 0.f;  // zg separable folds hsum later
 #pragma unroll
         for (int r = 0; r < kRPT; ++r)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
+            for (int j = 0; j < 4; ++j) acc[r][j] = init;
     }
 
     if constexpr (KIND == kZgSeparable) {

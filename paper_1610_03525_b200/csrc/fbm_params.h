@@ -98,7 +98,7 @@ struct FbmArgs {
     int32_t n_maps;
     int32_t epilogue;        // 0 none, 1 marble, 2 wood (texture.hpp:50-72, fused into the store)
     int32_t tma;             // set by the launcher: tile store through the output tensor map
-    int32_t pad0;
+    float hoff;              // -sum of the octave amplitudes (map_height offset, lattice.cuh)
     float tex_freq2pi;       // 2*pi*pattern_frequency
     float tex_gain;          // turbulence gain
     // Row LUT of the smoothstep order in use: for ppc = 2^k, entries
@@ -119,6 +119,8 @@ struct Fbm3Args {
     int32_t octaves;
     int32_t zero;
     uint64_t seed_key;
+    float hoff;         // -sum of the octave amplitudes (map_height offset, lattice.cuh)
+    int32_t pad;
     const float4* lut;  // row LUT (see FbmArgs)
     OctDev oct[kMaxOctaves];
 };

@@ -116,19 +116,22 @@ __device__ __forceinline__ float height_scaled(uint64_t packed) {
 
 // Map-path corner height from the top word of fmix64 only.  The final
 // xorshift (z ^= z >> 33) touches only the low word, and the second multiply
-// needs only its high word (mul.hi of the low words plus both cross terms),
-// with the sign flip (z ^ 2^63 = z + 2^63) folded into its addend; one
-// s32 -> f32 conversion then gives RN(floor(corner_height * 2^31)), i.e. the
-// height to |error| <= 2^-31 + half an fp32 ulp (heights are checked within
-// the north star's 1e-5 tolerance; the hash itself and tg_lattice_height_f32
-// stay bit-exact).  11 instructions per key against 14 for height_scaled.
+// needs only its high word (mul.hi of the low words plus both cross terms).
+// With u = that word, corner_height = (u + frac) * 2^-31 - 1, frac in [0, 1):
+// map_height returns float(u) (one u32 -> f32 conversion, |error| <= 2^-25 u)
+// and the kernels fold the -1 of every octave into one per-pixel constant
+// (FbmArgs::hoff), which is exact because every zero-gradient / generic cell
+// is an affine blend of its corner heights (weights summing to 1).  Heights
+// are thereby within 2^-24 * amp of the reference (checked against the north
+// star's 1e-5 tolerance; the hash itself and tg_lattice_height_f32 stay
+// bit-exact).  10 instructions per key against 14 for height_scaled.
 __device__ __forceinline__ float height_hi(uint64_t p) {
     uint32_t lo = static_cast<uint32_t>(p), hi = static_cast<uint32_t>(p >> 32);
     lo ^= hi >> 1;
     TG_MUL64(lo, hi, 0xED558CCD, 0xFF51AFD7);
     lo ^= hi >> 1;
-    int32_t t;
-    asm("{\n\t.reg .b32 q;\n\tmad.hi.u32 q, %1, 0x1A85EC53, 0x80000000;\n\t"
+    uint32_t t;
+    asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
         "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
         : "=r"(t)
         : "r"(lo), "r"(hi));
@@ -149,8 +152,8 @@ __device__ __forceinline__ void height_hi4(uint64_t p0, uint64_t p1, uint64_t p2
     for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        int32_t t;
-        asm("{\n\t.reg .b32 q;\n\tmad.hi.u32 q, %1, 0x1A85EC53, 0x80000000;\n\t"
+        uint32_t t;
+        asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
             "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
             : "=r"(t)
             : "r"(l[i]), "r"(h[i]));
@@ -158,20 +161,22 @@ __device__ __forceinline__ void height_hi4(uint64_t p0, uint64_t p1, uint64_t p2
     }
 }
 
-// The height representation of the map kernels: map_height(p) * kMapScale
-// is the corner height.  TG_MAP_HEIGHT_HI=0 selects the exactly rounded
-// height_scaled path (for A/B checks).
+// The height representation of the map kernels: the corner height is
+// map_height(p) * kMapScale + kMapOffset.  TG_MAP_HEIGHT_HI=0 selects the
+// exactly rounded height_scaled path (for A/B checks).
 #ifndef TG_MAP_HEIGHT_HI
 #define TG_MAP_HEIGHT_HI 1
 #endif
 #if TG_MAP_HEIGHT_HI
 constexpr float kMapScale = 0x1p-31f;
+constexpr bool kMapOffset = true;  // -1 per octave, folded into FbmArgs::hoff
 __device__ __forceinline__ float map_height(uint64_t p) { return height_hi(p); }
 __device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
     height_hi4(p0, p1, p2, p3, o);
 }
 #else
 constexpr float kMapScale = 0x1p-63f;
+constexpr bool kMapOffset = false;
 __device__ __forceinline__ float map_height(uint64_t p) { return height_scaled(p); }
 __device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
     height_scaled4(p0, p1, p2, p3, o);
