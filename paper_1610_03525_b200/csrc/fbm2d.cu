@@ -249,6 +249,88 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch
     }
 }
 
+// Corner grid of one aligned power-of-two octave (ppc = 2^SH <= 16) for a
+// 128 x 64 tile: (Wm + 1) x (Hm + 1) corners, Wm = 128 >> SH, Hm = 64 >> SH.
+// The Wm x Hm main block goes 4 consecutive corners per lane (four
+// independent hash chains, keys advanced by +K3, one 16-byte store per
+// channel), rows strided over the warps starting at warp `rot`; the last
+// column and row go one corner per thread starting at thread 32 * rot.
+template <int SH, int CH, class GV>
+__device__ __forceinline__ void fine_grid(float* g, int pitch, uint64_t p0, int warp, int lane, int tid, int rot,
+                                          GV& grid_value, const OctDev& od) {
+    constexpr int Wm = kTileW >> SH, Hm = kTileH >> SH;
+    constexpr int LSH = 5 - SH;                   // log2(lanes per corner row) = log2(Wm / 4)
+    constexpr int RSTEP = 8 << SH;                // corner rows per pass over the 8 warps
+    constexpr int NIT = (Hm + RSTEP - 1) / RSTEP;  // passes
+    const int wv = (warp - rot) & 7;
+    const int cg = lane & ((1 << LSH) - 1), rs = lane >> LSH;
+    const int cy0 = (wv << SH) + rs;
+    uint64_t p = p0 + static_cast<uint64_t>(4 * cg) * kIxMul + static_cast<uint64_t>(static_cast<uint32_t>(cy0)) * kIyMul;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const int cy = cy0 + it * RSTEP;
+        if (Hm % RSTEP == 0 || cy < Hm) {
+            float d[4][CH];
+            if constexpr (CH == 1) {
+                float h[4];
+                map_height4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) d[u][0] = h[u];
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) grid_value(add64(p, u * kIxMul), od, d[u]);
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+                *reinterpret_cast<float4*>(g + c * kGridCap + cy * pitch + 4 * cg) =
+                    make_float4(d[0][c], d[1][c], d[2][c], d[3][c]);
+        }
+        if (it + 1 < NIT) p = add64(p, static_cast<uint64_t>(RSTEP) * kIyMul);
+    }
+    constexpr int NE = Hm + 1 + Wm;  // last column (Hm + 1 corners) then last row (Wm)
+    for (int i = (tid - 32 * rot) & (kThreads - 1); i < NE; i += kThreads) {
+        const int cx = i <= Hm ? Wm : i - Hm - 1;
+        const int cy = i <= Hm ? i : Hm;
+        float d[CH];
+        grid_value(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                       static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul,
+                   od, d);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) g[c * kGridCap + cy * pitch + cx] = d[c];
+    }
+}
+
+// fine_grid with the shape decided at run time (same corner assignment).
+template <int CH, class GV>
+__device__ __forceinline__ void fine_grid_rt(int sh, float* g, int pitch, uint64_t p0, int warp, int lane, int tid,
+                                          int rot, GV& grid_value, const OctDev& od) {
+    const int Wm = kTileW >> sh, Hm = kTileH >> sh;
+    const int lsh = 5 - sh, rstep = 8 << sh;
+    const int wv = (warp - rot) & 7;
+    const int cg = lane & ((1 << lsh) - 1), rs = lane >> lsh;
+    const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
+    for (int cy = (wv << sh) + rs; cy < Hm; cy += rstep) {
+        const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
+        float d[4][CH];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) grid_value(add64(p, u * kIxMul), od, d[u]);
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+            *reinterpret_cast<float4*>(g + c * kGridCap + cy * pitch + 4 * cg) =
+                make_float4(d[0][c], d[1][c], d[2][c], d[3][c]);
+    }
+    for (int i = (tid - 32 * rot) & (kThreads - 1); i < Hm + 1 + Wm; i += kThreads) {
+        const int cx = i <= Hm ? Wm : i - Hm - 1;
+        const int cy = i <= Hm ? i : Hm;
+        float d[CH];
+        grid_value(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
+                       static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul,
+                   od, d);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) g[c * kGridCap + cy * pitch + cx] = d[c];
+    }
+}
+
 // zero-gradient cell rows r_begin.. of one cell: c0 = h00 + sy*dy goes into
 // the per-row accumulator (common to the 4 columns), the rest per pixel.
 // Zero-gradient cell in column form: with the column features
@@ -394,41 +476,22 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const uint64_t p0 = pack_xy(base, ix0, iy0);
         float* g = grid + od.goff;
         if (aligned && od.shift <= 4) {
-            // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc.  The main
-            // block goes 4 consecutive corners per lane (four independent hash
-            // chains, keys advanced by +K3, one 16-byte store); the last column
-            // and row go through the flat loop.
-            const int sh = od.shift;
-            const int Wm = kTW >> sh, Hm = kTH >> sh;
-            const int lsh = 5 - sh;  // log2(lanes per corner row) = log2(Wm / 4)
-            const int cg = lane & ((1 << lsh) - 1), rs = lane >> lsh;
-            const int rstep = (kThreads / 32) << sh;  // rows per pass over all warps
-            const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
-            for (int cy = (warp << sh) + rs; cy < Hm; cy += rstep) {
-                const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul;
-                if constexpr (kZg) {
-                    float h[4];
-                    map_height4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
-                    *reinterpret_cast<float4*>(g + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
-                } else {
-                    float d[4][CH];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) grid_value(add64(p, u * kIxMul), od, d[u]);
-#pragma unroll
-                    for (int c = 0; c < CH; ++c)
-                        *reinterpret_cast<float4*>(g + c * kGridCap + cy * pitch + 4 * cg) =
-                            make_float4(d[0][c], d[1][c], d[2][c], d[3][c]);
-                }
-            }
-            for (int i = tid; i < Hm + 1 + Wm; i += kThreads) {
-                const int cx = i <= Hm ? Wm : i - Hm - 1;
-                const int cy = i <= Hm ? i : Hm;
-                float d[CH];
-                grid_value(p0 + static_cast<uint64_t>(static_cast<uint32_t>(cx)) * kIxMul +
-                               static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul,
-                           od, d);
-#pragma unroll
-                for (int c = 0; c < CH; ++c) g[c * kGridCap + cy * pitch + cx] = d[c];
+            // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc, shapes
+            // fixed at compile time per ppc.  The starting warp / thread
+            // rotates with the list position so the small grids (ppc 8, 16)
+            // and the edge lists of successive octaves land on different warps.
+            const int rot = q & 7;
+            if constexpr (KIND == kGeneric) {
+                // one runtime-shaped copy: five specialisations of the 3-lane
+                // corner hash (two with sincos) cost more than they save
+                // (measured 321 -> 417 us at config 3)
+                fine_grid_rt<CH>(od.shift, g, pitch, p0, warp, lane, tid, rot, grid_value, od);
+            } else switch (od.shift) {
+                case 0: fine_grid<0, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
+                case 1: fine_grid<1, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
+                case 2: fine_grid<2, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
+                case 3: fine_grid<3, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
+                default: fine_grid<4, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
             }
         } else {
             // Any other shape: flat corner list, four hash chains per thread.
