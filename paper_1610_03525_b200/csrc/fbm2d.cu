@@ -526,7 +526,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     float racc[kRPT];  // per-row terms common to the 4 columns (Perlin/generic block modes)
     // term common to all 32 pixels (zg block modes), starting from the
     // map_height offset of every octave (lattice.cuh)
-    float hsum = kMapOffset && KIND != kPerlin ? args.hoff : 0.f;
+    float hsum = kMapOffset && KIND != kPerlin ? kMapOffsetUnits * args.hoff : 0.f;
     float cacc[4] = {0.f, 0.f, 0.f, 0.f};  // per-column terms (zg block modes)
 #pragma unroll
     for (int r = 0; r < kRPT; ++r) racc[r] = 0.f;

@@ -220,7 +220,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     for (int z = 0; z < kTZ; ++z) {
         racc[z] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[z][j] = kMapOffset ? a.hoff : 0.f;  // map_height offsets
+        for (int j = 0; j < 4; ++j) acc[z][j] = kMapOffset ? kMapOffsetUnits * a.hoff : 0.f;  // map_height offsets
     }
 
     for (int o = 0; o < a.octaves; ++o) {

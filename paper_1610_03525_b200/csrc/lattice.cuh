@@ -117,15 +117,13 @@ __device__ __forceinline__ float height_scaled(uint64_t packed) {
 // Map-path corner height from the top word of fmix64 only.  The final
 // xorshift (z ^= z >> 33) touches only the low word, and the second multiply
 // needs only its high word (mul.hi of the low words plus both cross terms).
-// With u = that word, corner_height = (u + frac) * 2^-31 - 1, frac in [0, 1):
-// map_height returns float(u) (one u32 -> f32 conversion, |error| <= 2^-25 u)
-// and the kernels fold the -1 of every octave into one per-pixel constant
-// (FbmArgs::hoff), which is exact because every zero-gradient / generic cell
-// is an affine blend of its corner heights (weights summing to 1).  Heights
-// are thereby within 2^-24 * amp of the reference (checked against the north
-// star's 1e-5 tolerance; the hash itself and tg_lattice_height_f32 stay
-// bit-exact).  10 instructions per key against 14 for height_scaled.
-__device__ __forceinline__ float height_hi(uint64_t p) {
+// With u = that word, corner_height = (u + frac) * 2^-31 - 1, frac in [0, 1).
+// The kernels fold the constant part of every octave (-amp after the scale)
+// into one per-pixel offset (FbmArgs::hoff), which is exact because every
+// zero-gradient / generic cell is an affine blend of its corner heights
+// (weights summing to 1).  The hash itself and tg_lattice_height_f32 stay
+// bit-exact; map heights are checked against the north star's 1e-5 tolerance.
+__device__ __forceinline__ uint32_t hash_top_word(uint64_t p) {
     uint32_t lo = static_cast<uint32_t>(p), hi = static_cast<uint32_t>(p >> 32);
     lo ^= hi >> 1;
     TG_MUL64(lo, hi, 0xED558CCD, 0xFF51AFD7);
@@ -135,11 +133,12 @@ __device__ __forceinline__ float height_hi(uint64_t p) {
         "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
         : "=r"(t)
         : "r"(lo), "r"(hi));
-    return static_cast<float>(t);
+    return t;
 }
 
 // Four independent keys in lock step (see height_scaled4).
-__device__ __forceinline__ void height_hi4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&out)[4]) {
+__device__ __forceinline__ void hash_top_word4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3,
+                                               uint32_t (&out)[4]) {
     uint32_t l[4] = {static_cast<uint32_t>(p0), static_cast<uint32_t>(p1), static_cast<uint32_t>(p2),
                      static_cast<uint32_t>(p3)};
     uint32_t h[4] = {static_cast<uint32_t>(p0 >> 32), static_cast<uint32_t>(p1 >> 32),
@@ -151,32 +150,40 @@ __device__ __forceinline__ void height_hi4(uint64_t p0, uint64_t p1, uint64_t p2
 #pragma unroll
     for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        uint32_t t;
+    for (int i = 0; i < 4; ++i)
         asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
             "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
-            : "=r"(t)
+            : "=r"(out[i])
             : "r"(l[i]), "r"(h[i]));
-        out[i] = static_cast<float>(t);
-    }
 }
 
 // The height representation of the map kernels: the corner height is
-// map_height(p) * kMapScale + kMapOffset.  TG_MAP_HEIGHT_HI=0 selects the
-// exactly rounded height_scaled path (for A/B checks).
+// map_height(p) * kMapScale - kMapOffsetUnits (the second term folded into
+// FbmArgs::hoff = -sum(amp), scaled by kMapOffsetUnits in the kernels).
+//   TG_MAP_HEIGHT_HI=1 (default): f = float(u) (one I2FP), height =
+//     f * 2^-31 - 1, |error| <= 2^-24.  10 instructions per key.  (Building
+//     f in [1, 2) from u's high 23 bits with one integer LEA.HI instead
+//     measured the same.)
+//   TG_MAP_HEIGHT_HI=0: the exactly rounded height_scaled path, 14 per key.
 #ifndef TG_MAP_HEIGHT_HI
 #define TG_MAP_HEIGHT_HI 1
 #endif
 #if TG_MAP_HEIGHT_HI
 constexpr float kMapScale = 0x1p-31f;
-constexpr bool kMapOffset = true;  // -1 per octave, folded into FbmArgs::hoff
-__device__ __forceinline__ float map_height(uint64_t p) { return height_hi(p); }
+constexpr float kMapOffsetUnits = 1.0f;
+__device__ __forceinline__ float top_word_height(uint32_t t) { return static_cast<float>(t); }
+constexpr bool kMapOffset = true;
+__device__ __forceinline__ float map_height(uint64_t p) { return top_word_height(hash_top_word(p)); }
 __device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
-    height_hi4(p0, p1, p2, p3, o);
+    uint32_t t[4];
+    hash_top_word4(p0, p1, p2, p3, t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = top_word_height(t[i]);
 }
 #else
 constexpr float kMapScale = 0x1p-63f;
 constexpr bool kMapOffset = false;
+constexpr float kMapOffsetUnits = 0.0f;
 __device__ __forceinline__ float map_height(uint64_t p) { return height_scaled(p); }
 __device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
     height_scaled4(p0, p1, p2, p3, o);
