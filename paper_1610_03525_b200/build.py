@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -40,9 +41,10 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if not force and out is None and not _stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
+    objdir = tempfile.mkdtemp(prefix="tgobj_", dir=LIB_DIR)  # private: concurrent builds of variants
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIB_DIR, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
@@ -62,6 +64,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     os.replace(tmp, target)
     for o in objs:
         os.remove(o)
+    os.rmdir(objdir)
     return target
 
 

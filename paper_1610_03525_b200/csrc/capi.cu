@@ -106,6 +106,7 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
     const double R = static_cast<double>(c->resolution);
     const double w = c->has_gradient_weight ? c->gradient_weight : c->base_amplitude / 100.0;
     const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
+    const bool paper = c->method == TG_METHOD_ZG_PAPER;
     int goff = 0, slot = 0;
     for (int o = 0; o < c->octaves; ++o) {
         tg_octave_spec os;
@@ -291,6 +292,8 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     a->hoff = amp_offset(a->oct, c->octaves);
     // mode-homogeneous octave lists (fbm_params.h OctGroup)
     const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
+    const bool paper = c->method == TG_METHOD_ZG_PAPER;
+    for (int o = 0; o < c->octaves; ++o) a->oct[o].cslot = -1;
     for (int o = 0; o < c->octaves; ++o) {
         const tg::OctDev& d = a->oct[o];
         auto push = [&](int g) { a->group[g][a->ngroup[g]++] = static_cast<int8_t>(o); };
@@ -299,7 +302,13 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
         if (has_grid) push(d.lut_off >= 0 && d.mode != tg::kModeGrid && d.ncx * d.ncy <= 32 ? tg::kGProCoarse
                                                                                             : tg::kGProFine);
         if (d.mode == tg::kModeSubInt) push(tg::kGSub);
-        else if (zg && d.mode == tg::kModeBlock && d.shift >= 3) push(tg::kGBlk8);
+        else if (zg && d.mode == tg::kModeBlock && d.shift >= 3) {
+            // ppc >= 32 on a 128 x 64 tile: at most 4 x 2 cells, 15 corners
+            const bool tile_terms = paper && d.shift >= 5 && tg::fbm2d_tile_h() == 64 && d.ncx * d.ncy <= 32 &&
+                                    a->ngroup[tg::kGBlkT] < tg::kMaxCellSlots;
+            if (tile_terms) a->oct[o].cslot = a->ngroup[tg::kGBlkT];
+            push(tile_terms ? tg::kGBlkT : tg::kGBlk8);
+        }
         else if (zg && d.mode == tg::kModeBlock && d.shift == 2) push(tg::kGBlk4);
         else if (d.mode == tg::kModeBlock2) push(tg::kGBlk2);
         else if (d.mode == tg::kModePpc1) push(tg::kGPpc1);

@@ -222,10 +222,18 @@ struct TabSlot {
     float4 rowF[kTH];   // y, S(y), S(y) - y, cell row relative (bits)
 };
 
-// LEAN kernels (no general octaves) need no sampling tables.
+// LEAN kernels (no general octaves) need no sampling tables.  The zg paper
+// kernels add the per-tile column / row term arrays (kGBlkT) after the grid.
+template <int KIND, bool LEAN>
+constexpr size_t smem_grid_end() {
+    return (LEAN ? 0 : sizeof(TabSlot) * kTabSlots) + sizeof(float) * Traits<KIND>::kCh * kGridCap;
+}
+// floats: Cw[2][128], C1[2][128], Rw[4][64], R1[4][64], then the kGBlkT
+// octaves' cell parameters (h00, dx, dy, a) x 8 cells per slot
+constexpr int kFeat = 4 * 256 + 4 * 8 * kMaxCellSlots;
 template <int KIND, bool LEAN>
 constexpr size_t smem_bytes() {
-    return (LEAN ? 0 : sizeof(TabSlot) * kTabSlots) + sizeof(float) * Traits<KIND>::kCh * kGridCap;
+    return smem_grid_end<KIND, LEAN>() + (KIND == kZgPaper ? sizeof(float) * kFeat : 0);
 }
 
 // q*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
@@ -374,6 +382,15 @@ __device__ __forceinline__ void zg_cols(float (&acc)[kRPT][4], float (&cacc)[4],
     }
 }
 
+// Timing experiments only: TG_SKIP is a bit mask of octave lists to skip
+// (1 fine grids, 2 lattice-point octaves, 4 per-thread block octaves, 8
+// per-tile block octaves, 16 ppc-4, 32 ppc-2, 64 ppc-1); 0 in every build
+// that produces maps.
+#ifndef TG_SKIP
+#define TG_SKIP 0
+#endif
+#define TG_NG(g, bit) ((TG_SKIP & (bit)) ? 0 : args.ngroup[g])
+
 #ifndef TG_ZG_MIN_BLOCKS
 #define TG_ZG_MIN_BLOCKS 3
 #endif
@@ -424,8 +441,21 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     // (a) coarse aligned octaves (<= 32 corners): one warp per octave.
     for (int q = warp; q < args.ngroup[kGProCoarse]; q += kThreads / 32) {
         const OctDev& od = args.oct[args.group[kGProCoarse][q]];
-        if (lane < od.ncx * od.ncy) {
-            const int cy = lane / od.ncx, cx = lane - cy * od.ncx;
+        const int cy = lane / od.ncx, cx = lane - cy * od.ncx;
+        if (KIND == kZgPaper && kRPT == 8 && od.cslot >= 0) {
+            // kGBlkT octave: the cells' (h00, dx, dy, a) x amp straight from
+            // the lanes' corners (lane = cy * ncx + cx), no grid
+            float h = map_height(pack_xy(seed_key + od.oct_key, (tx0 >> od.shift) + cx, (ty0 >> od.shift) + cy));
+            h *= od.amp * kMapScale;
+            const float h10 = __shfl_down_sync(0xffffffffu, h, 1);
+            const float h01 = __shfl_down_sync(0xffffffffu, h, od.ncx);
+            const float h11 = __shfl_down_sync(0xffffffffu, h, od.ncx + 1);
+            if (cx < od.ncx - 1 && cy < od.ncy - 1) {
+                float4* cp = reinterpret_cast<float4*>(smem_raw + smem_grid_end<KIND, LEAN>()) + 256;
+                const float dy = h01 - h;
+                cp[od.cslot * 8 + cy * (od.ncx - 1) + cx] = make_float4(h, h10 - h, dy, (h11 - h10) - dy);
+            }
+        } else if (lane < od.ncx * od.ncy) {
             float d[CH];
             grid_value(pack_xy(seed_key + od.oct_key, (tx0 >> od.shift) + cx, (ty0 >> od.shift) + cy), od, d);
 #pragma unroll
@@ -433,7 +463,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         }
     }
     // (b) everything else with a grid
-    for (int q = 0; q < args.ngroup[kGProFine]; ++q) {
+    for (int q = 0; q < TG_NG(kGProFine, 1); ++q) {
         const OctDev& od = args.oct[args.group[kGProFine][q]];
         const uint64_t base = seed_key + od.oct_key;
         const bool aligned = od.lut_off >= 0;  // power-of-two ppc on the aligned tile grid
@@ -546,7 +576,78 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         for (int r = 0; r < kRPT; ++r) R0[r] = R1[r] = 0.f;
         const float* lutS = reinterpret_cast<const float*>(args.lut + kLutN4);  // S(x)
         const float* lutD = lutS + kLutN4;                                       // S(x) - x
-        for (int q = 0; q < args.ngroup[kGBlk8]; ++q) {
+        if constexpr (kRPT == 8) {
+            if (TG_NG(kGBlkT, 8) > 0) {  // uniform per launch
+                // ppc >= 32: a 128 x 64 tile spans at most 4 x 2 cells, so in
+                // tile coordinates (X, Y) each octave is
+                //   v = Cw(X, cr) + Y*C1(X, cr) + Rw(Y, cc) + X*R1(Y, cc)
+                // with x = xc + X/ppc, y = yc + Y/ppc inside cell (cc, cr):
+                //   Cw = h00 + Sx*dx + (a*yc)*(Sx - x), C1 = (a/ppc)*(Sx - x),
+                //   Rw = Sy*(dy + a*xc),                R1 = (a/ppc)*Sy.
+                // Cells nest, so every octave's (cc, cr) follows from the
+                // ppc-32 cell: thread t builds the column entry (X = t % 128,
+                // ppc-32 cell row t / 128) and the row entry (Y = t % 64,
+                // ppc-32 cell column t / 64), summed over the whole list.
+                float* feat = reinterpret_cast<float*>(smem_raw + smem_grid_end<KIND, LEAN>());
+                const int X = tid & 127, crP = tid >> 7, Y = tid & 63, ccP = tid >> 6;
+                float cw = 0.f, c1 = 0.f, rw = 0.f, r1 = 0.f;
+                const float4* cpar = reinterpret_cast<const float4*>(feat) + 256;
+                for (int q = 0; q < args.ngroup[kGBlkT]; ++q) {
+                    const OctDev& od = args.oct[args.group[kGBlkT][q]];
+                    const int sh = od.shift, mask = od.ppc - 1, cw1 = od.ncx - 1;
+                    const float inv = od.inv_ppc;
+                    const int tmx = static_cast<int>(tx0 & mask), tmy = static_cast<int>(ty0 & mask);
+                    const float4* cq = cpar + od.cslot * 8;
+                    {  // column entry
+                        const int cx = X >> sh, cr = (crP << 5) >> sh;
+                        const float4 cp = cq[cr * cw1 + cx];  // h00, dx, dy, a
+                        const int mx = (tmx + X) & mask;
+                        const float sx = __ldg(lutS + od.ppc + mx), d = __ldg(lutD + od.ppc + mx);
+                        const float yc = (static_cast<float>(tmy - (cr << sh)) + 0.5f) * inv;
+                        cw += fmaf(cp.w * yc, d, fmaf(sx, cp.y, cp.x));
+                        c1 = fmaf(cp.w * inv, d, c1);
+                    }
+                    {  // row entry
+                        const int cc = (ccP << 5) >> sh, cr = Y >> sh;
+                        const float4 cp = cq[cr * cw1 + cc];
+                        const int my = (tmy + Y) & mask;
+                        const float sy = __ldg(lutS + od.ppc + my);
+                        const float xc = (static_cast<float>(tmx - (cc << sh)) + 0.5f) * inv;
+                        rw = fmaf(sy, fmaf(cp.w, xc, cp.z), rw);
+                        r1 = fmaf(cp.w * inv, sy, r1);
+                    }
+                }
+                feat[tid] = cw;
+                feat[256 + tid] = c1;
+                feat[512 + tid] = rw;
+                feat[768 + tid] = r1;
+                __syncthreads();
+                // the thread's block: X = c0 + j, Y = r0 + r (block-local c = j, r = r)
+                const float* fc = feat + (r0 >> 5) * 128 + c0;
+                const float* fr = feat + 512 + (c0 >> 5) * 64 + r0;
+                const float4 cw4 = *reinterpret_cast<const float4*>(fc);
+                const float4 c14 = *reinterpret_cast<const float4*>(fc + 256);
+                const float cwa[4] = {cw4.x, cw4.y, cw4.z, cw4.w}, c1a[4] = {c14.x, c14.y, c14.z, c14.w};
+                const float fr0 = static_cast<float>(r0), fc0 = static_cast<float>(c0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    C0[j] = fmaf(fr0, c1a[j], cwa[j]);
+                    C1[j] = c1a[j];
+                }
+#pragma unroll
+                for (int r4 = 0; r4 < kRPT; r4 += 4) {
+                    const float4 rw4 = *reinterpret_cast<const float4*>(fr + r4);
+                    const float4 r14 = *reinterpret_cast<const float4*>(fr + 256 + r4);
+                    const float rwa[4] = {rw4.x, rw4.y, rw4.z, rw4.w}, r1a[4] = {r14.x, r14.y, r14.z, r14.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        R0[r4 + i] = fmaf(fc0, r1a[i], rwa[i]);
+                        R1[r4 + i] = r1a[i];
+                    }
+                }
+            }
+        }
+        for (int q = 0; q < TG_NG(kGBlk8, 4); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk8][q]];
             const int sh = od.shift, mask = od.ppc - 1;
             const int xo = static_cast<int>(tx0 & mask) + c0;
@@ -600,7 +701,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
 
     if constexpr (KIND == kZgSeparable) {
         // power-of-two ppc >= 8: the 4 x 8 block lies in one cell
-        for (int q = 0; q < args.ngroup[kGBlk8]; ++q) {
+        for (int q = 0; q < TG_NG(kGBlk8, 4); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk8][q]];
             const int sh = od.shift, mask = od.ppc - 1;
             const float4* L = args.lut + od.lut_off;
@@ -622,7 +723,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     }
     if constexpr (kZg) {
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
-        for (int q = 0; q < args.ngroup[kGBlk4]; ++q) {
+        for (int q = 0; q < TG_NG(kGBlk4, 16); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk4][q]];
             const float4* L = args.lut + od.lut_off;  // 4 entries: x = 1/8, 3/8, 5/8, 7/8
             const int pitch = od.pitch;
@@ -655,7 +756,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
 
     // ppc == 2: columns (0,1) | (2,3) are two cells at x = 0.25, 0.75; rows
     // pair up the same way; 3 corners per corner row.
-    for (int q = 0; q < args.ngroup[kGBlk2]; ++q) {
+    for (int q = 0; q < TG_NG(kGBlk2, 32); ++q) {
         const OctDev& od = args.oct[args.group[kGBlk2][q]];
         const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
         const int pitch = od.pitch;
@@ -695,7 +796,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         }
     }
     // ppc == 1 (x = y = 1/2)
-    for (int q = 0; q < args.ngroup[kGPpc1]; ++q) {
+    for (int q = 0; q < TG_NG(kGPpc1, 64); ++q) {
         const OctDev& od = args.oct[args.group[kGPpc1][q]];
         const int pitch = od.pitch;
         const float* g = grid + od.goff + r0 * pitch + c0;
@@ -746,7 +847,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     // lattice-point octaves: zg and generic contribute h(ix, iy) exactly,
     // Perlin exactly 0 (SURVEY §8c "exact shortcuts")
     if constexpr (KIND != kPerlin) {
-        for (int q = 0; q < args.ngroup[kGSub]; ++q) {
+        for (int q = 0; q < TG_NG(kGSub, 2); ++q) {
             const OctDev& od = args.oct[args.group[kGSub][q]];
             const float amp = od.amp * kMapScale;  // exact power-of-two rescale
             const int64_t k = od.k, half = od.k >> 1;

@@ -24,6 +24,7 @@ enum OctaveClass : int32_t {
 enum KernelKind : int32_t { kZgPaper = 0, kZgSeparable = 1, kGeneric = 2, kPerlin = 3, kOpenSimplex = 4 };
 
 constexpr int kMaxOctaves = 32;
+constexpr int kMaxCellSlots = 10;  // kGBlkT octaves with per-tile cell parameters (8 cells each)
 constexpr int kMaxBatch = 64;
 
 // 2D tile geometry and per-CTA shared-memory budget (fbm2d.cu).
@@ -66,7 +67,9 @@ struct OctDev {
     int32_t goff;      // grid offset (floats per channel, multiple of 4)
     int32_t tslot;     // sampling-table slot (kModeGrid) or -1
     int32_t lut_off;   // offset of this ppc's row LUT (aligned modes) or -1
-    int32_t pad;
+    int32_t pad;       // 3D: corner grid depth (ncz)
+    int32_t cslot;     // kGBlkT: slot of the octave's per-tile cell parameters, else -1
+    int32_t pad2;
     double ratio;      // freq / R (OpenSimplex sample spacing), set by its launcher
 };
 
@@ -83,7 +86,8 @@ enum OctGroup : int32_t {
     kGPpc1 = 5,       // zg, ppc == 1
     kGSub = 6,        // lattice-point octaves
     kGGen = 7,        // everything else (Perlin/generic cells, general octaves)
-    kNumGroups = 8
+    kGBlkT = 8,       // zg paper, power-of-two ppc >= 32: column / row terms built once per tile
+    kNumGroups = 9
 };
 
 struct FbmArgs {
