@@ -191,6 +191,32 @@ def hashes_per_launch(res: int, f0: int, octaves: int, tw: int = 128, th: int = 
     return total
 
 
+# Measured on B200 by tools/micro/pipe_rates.cu (warp-instructions per SMSP
+# per cycle): IMAD 0.5, IMAD.WIDE.U32 / IMAD.HI.U32 0.25, SHF/LOP3 0.5,
+# FFMA ~1.  One map-path lattice hash (lattice.cuh hash_top_word) is
+# IMAD.WIDE + 2 IMAD + IMAD.HI + 2 IMAD = 16 IMAD-pipe cycles per warp.
+IMAD_CYCLES_PER_WARP_HASH = 16
+SMSP_PER_SM, N_SM = 4, 148
+
+
+def integer_floor(hashes: int, launch_s: float, sm_mhz) -> dict:
+    """The bound the bit-exact hash alone puts on a launch: its 64-bit
+    multiplies on the IMAD pipe, all SMSPs busy, at the sampled SM clock; and
+    the issue bound of the kernel's executed instruction count from the
+    committed ncu capture."""
+    mhz = float(sm_mhz or 1965.0)
+    hash_s = hashes / 32.0 * IMAD_CYCLES_PER_WARP_HASH / (SMSP_PER_SM * N_SM) / (mhz * 1e6)
+    out = {"hash_imad_floor_us": hash_s * 1e6, "frac_of_launch": hash_s / launch_s,
+           "note": "hashes x 16 IMAD-pipe cycles per warp-hash / (592 SMSPs x clock); "
+                   "rates from tools/micro/pipe_rates.cu"}
+    inst = (traffic_summary() or {}).get("sm_inst_executed")
+    if inst:
+        issue_s = float(inst) / (SMSP_PER_SM * N_SM) / (mhz * 1e6)
+        out.update({"issue_floor_us": issue_s * 1e6, "issue_frac_of_launch": issue_s / launch_s,
+                    "issue_note": "ncu executed warp-instructions / (592 SMSPs x 1 issue/cycle x clock)"})
+    return out
+
+
 def measured_hbm_gbs() -> float:
     """HBM bandwidth from the driver-written MEASURED_PEAKS.json, else the
     B200 profiling recipe's fallback."""
@@ -418,7 +444,9 @@ def main() -> None:
                          "issue_slots_busy_pct_ncu": (traffic_summary() or {}).get("issue_active_pct"),
                          "issue_note": "the bit-exact 64-bit lattice hash is integer work outside the 7-flop "
                                        "convention; issue-slot utilisation of the same kernel from the committed "
-                                       "ncu capture (profiles/ncu_summary.json)"},
+                                       "ncu capture (profiles/ncu_summary.json)",
+                         "integer_floor": integer_floor(hashes_per_launch(R, F0, OCTAVES), avg_launch_s,
+                                                        clk.summary().get("sm_mhz"))},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(ccfg),
                     "d2h_bytes_per_step": R * R * 8, "steps": e2e_steps,
                     "ms_per_step_median": statistics.median(e2e_each) * 1e3,
