@@ -106,7 +106,6 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
     const double R = static_cast<double>(c->resolution);
     const double w = c->has_gradient_weight ? c->gradient_weight : c->base_amplitude / 100.0;
     const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
-    const bool paper = c->method == TG_METHOD_ZG_PAPER;
     int goff = 0, slot = 0;
     for (int o = 0; o < c->octaves; ++o) {
         tg_octave_spec os;
@@ -290,6 +289,22 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
     plan_octaves(c, gmax, a->oct, true);
     a->hoff = amp_offset(a->oct, c->octaves);
+    for (int o = 0; o < c->octaves; ++o) {  // per-launch key constants (fbm_params.h OctDev::key0)
+        tg::OctDev& d = a->oct[o];
+        const uint64_t tx = static_cast<uint64_t>(a->tile_x0), ty = static_cast<uint64_t>(a->tile_y0);
+        if (d.mode == tg::kModeSubInt) {
+            const uint64_t k = static_cast<uint64_t>(d.k), h = k >> 1;
+            d.kx = k * tg::kIxMul;
+            d.ky = k * tg::kIyMul;
+            d.key0 = d.oct_key + (tx * k + h) * tg::kIxMul + (ty * k + h) * tg::kIyMul;
+        } else if (d.lut_off >= 0 && d.shift >= 0 && d.shift <= 4) {
+            const int sh = d.shift;
+            d.kx = static_cast<uint64_t>(tg::kTileW >> sh) * tg::kIxMul;
+            d.ky = static_cast<uint64_t>(tg::fbm2d_tile_h() >> sh) * tg::kIyMul;
+            d.key0 = d.oct_key + static_cast<uint64_t>(a->tile_x0 >> sh) * tg::kIxMul +
+                     static_cast<uint64_t>(a->tile_y0 >> sh) * tg::kIyMul;
+        }
+    }
     // mode-homogeneous octave lists (fbm_params.h OctGroup)
     const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
     const bool paper = c->method == TG_METHOD_ZG_PAPER;

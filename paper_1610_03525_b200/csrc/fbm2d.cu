@@ -503,9 +503,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             }
         }
         const int pitch = od.pitch;
-        const uint64_t p0 = pack_xy(base, ix0, iy0);
         float* g = grid + od.goff;
         if (aligned && od.shift <= 4) {
+            const uint64_t p0 = seed_key + od.key0 + static_cast<uint64_t>(blockIdx.x) * od.kx +
+                                static_cast<uint64_t>(blockIdx.y) * od.ky;
             // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc, shapes
             // fixed at compile time per ppc.  The starting warp / thread
             // rotates with the list position so the small grids (ppc 8, 16)
@@ -525,6 +526,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             }
         } else {
             // Any other shape: flat corner list, four hash chains per thread.
+            const uint64_t p0 = pack_xy(base, ix0, iy0);
             const int n = ncx * ncy;
             const float rcp = 1.0f / static_cast<float>(ncx);
             for (int i0 = tid; i0 < n; i0 += 4 * kThreads) {
@@ -850,12 +852,14 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         for (int q = 0; q < TG_NG(kGSub, 2); ++q) {
             const OctDev& od = args.oct[args.group[kGSub][q]];
             const float amp = od.amp * kMapScale;  // exact power-of-two rescale
-            const int64_t k = od.k, half = od.k >> 1;
+            // key(gx, gy) = seed*K1 + oct*K2 + (gx*k + k/2)*K3 + (gy*k + k/2)*K4,
+            // tile / thread offsets as 32-bit multiples of the per-launch steps
             uint64_t X[4];
+            X[0] = static_cast<uint64_t>(blockIdx.x * kTW + c0) * od.kx;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) X[j] = static_cast<uint64_t>((tx0 + c0 + j) * k + half) * kIxMul;
-            uint64_t Y = seed_key + od.oct_key + static_cast<uint64_t>((ty0 + r0) * k + half) * kIyMul;
-            const uint64_t dY = static_cast<uint64_t>(k) * kIyMul;
+            for (int j = 1; j < 4; ++j) X[j] = add64(X[j - 1], od.kx);
+            uint64_t Y = seed_key + od.key0 + static_cast<uint64_t>(blockIdx.y * kTH + r0) * od.ky;
+            const uint64_t dY = od.ky;
 #pragma unroll
             for (int r = 0; r < kRPT; ++r) {
                 float h[4];

@@ -70,6 +70,13 @@ struct OctDev {
     int32_t pad;       // 3D: corner grid depth (ncz)
     int32_t cslot;     // kGBlkT: slot of the octave's per-tile cell parameters, else -1
     int32_t pad2;
+    // per-launch lattice-key constants (2D, build_args): the packed key of a
+    // tile's first corner / lattice point is seed*K1 + key0 + bx*kx + by*ky
+    //   lattice-point octaves: key0 = oct*K2 + (tile_x0*k + k/2)*K3 + (tile_y0*k + k/2)*K4,
+    //                          kx = k*K3 (per pixel column), ky = k*K4 (per pixel row)
+    //   aligned ppc <= 16:     key0 = oct*K2 + (tile_x0 >> s)*K3 + (tile_y0 >> s)*K4,
+    //                          kx = (128 >> s)*K3 (per tile), ky = (64 >> s)*K4 (per tile)
+    uint64_t key0, kx, ky;
     double ratio;      // freq / R (OpenSimplex sample spacing), set by its launcher
 };
 
