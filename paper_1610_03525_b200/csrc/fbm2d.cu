@@ -682,13 +682,54 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 }
             }
         }
+        // ppc == 4 in the same separated form.  The thread's 4 columns are one
+        // cell (x = 1/8 + c/4); rows 0-3 lie in cell row A, rows 4-7 in B
+        // (y = 1/8 + r/4 in A, -7/8 + r/4 in B).  The row terms take each
+        // half's own cell; the column terms of B differ from A's by D0, D1,
+        // added to rows 4-7 only.
+        float D0[4] = {0.f, 0.f, 0.f, 0.f}, D1[4] = {0.f, 0.f, 0.f, 0.f};
+        static_assert(kRPT == 8, "ppc-4 blocks assume 8 rows per thread (two cell rows)");
+        for (int q = 0; q < TG_NG(kGBlk4, 16); ++q) {
+            const OctDev& od = args.oct[args.group[kGBlk4][q]];
+            const float4* L = args.lut + od.lut_off;  // 4 entries: x = 1/8, 3/8, 5/8, 7/8
+            const int pitch = od.pitch;
+            const float* g = grid + od.goff + (r0 >> 2) * pitch + (c0 >> 2);
+            const float amp = od.amp * kMapScale;
+            const float a0 = amp * g[0], a1 = amp * g[1];
+            const float b0 = amp * g[pitch], b1 = amp * g[pitch + 1];
+            const float e0 = amp * g[2 * pitch], e1 = amp * g[2 * pitch + 1];
+            const float dyA = b0 - a0, aA = (b1 - a1) - dyA, dxA = a1 - a0;
+            const float dyB = e0 - b0, aB = (e1 - b1) - dyB, dxB = b1 - b0;
+            const float qA = 0.25f * aA, qB = 0.25f * aB;
+            float sv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float4 e = L[j];
+                sv[j] = e.y;
+                const float cA = fmaf(0.125f * aA, e.z, fmaf(e.y, dxA, a0));
+                const float cB = fmaf(-0.875f * aB, e.z, fmaf(e.y, dxB, b0));
+                C0[j] += cA;
+                D0[j] += cB - cA;
+                C1[j] = fmaf(qA, e.z, C1[j]);
+                D1[j] = fmaf(qB - qA, e.z, D1[j]);
+            }
+            const float kA = fmaf(0.125f, aA, dyA), kB = fmaf(0.125f, aB, dyB);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                R0[r] = fmaf(sv[r], kA, R0[r]);
+                R1[r] = fmaf(sv[r], qA, R1[r]);
+                R0[r + 4] = fmaf(sv[r], kB, R0[r + 4]);
+                R1[r + 4] = fmaf(sv[r], qB, R1[r + 4]);
+            }
+        }
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
             const float rr = R0[r] + hsum;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 float v = C0[j] + rr;
-                if (r) v = fmaf(static_cast<float>(r), C1[j], v);
+                if (r >= 4) v += D0[j];
+                if (r) v = fmaf(static_cast<float>(r), r >= 4 ? C1[j] + D1[j] : C1[j], v);
                 if (j) v = fmaf(static_cast<float>(j), R1[r], v);
                 acc[r][j] = v;
             }
@@ -723,7 +764,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                                       amp * g[od.pitch], amp * g[od.pitch + 1]);
         }
     }
-    if constexpr (kZg) {
+    if constexpr (KIND == kZgSeparable) {
         // ppc == 4: the thread's 4 columns are one cell; rows 0-3 / 4-7 two cell rows
         for (int q = 0; q < TG_NG(kGBlk4, 16); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk4][q]];
