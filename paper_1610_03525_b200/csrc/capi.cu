@@ -329,6 +329,30 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
         else if (d.mode == tg::kModePpc1) push(tg::kGPpc1);
         else push(tg::kGGen);
     }
+    // aligned ppc <= 16 grids leave the kGProFine list for the per-ppc slots
+    for (int sl = 0; sl < tg::kFineSlots; ++sl) a->fine[sl].goff = -1;
+    {
+        int n = 0, nspec = 0;
+        for (int q = 0; q < a->ngroup[tg::kGProFine]; ++q) {
+            const int o = a->group[tg::kGProFine][q];
+            const tg::OctDev& d = a->oct[o];
+            const int sh = d.shift;
+            if (c->method != TG_METHOD_GENERIC && d.mode != tg::kModeGrid && d.lut_off >= 0 && sh >= 0 && sh < tg::kFineSlots &&
+                a->fine[sh].goff < 0) {  // (grid-mode octaves also build sampling tables)
+                tg::FineDev& f = a->fine[sh];
+                f.key0 = d.key0;
+                f.kx = d.kx;
+                f.ky = d.ky;
+                f.goff = d.goff;
+                f.pitch = d.pitch;
+                f.rot = (nspec++) & 7;
+                f.oct = o;
+            } else {
+                a->group[tg::kGProFine][n++] = static_cast<int8_t>(o);
+            }
+        }
+        a->ngroup[tg::kGProFine] = n;
+    }
     a->lut = tg::row_lut(order_of(c));
     if (!a->lut) return fail(TG_EDEVICE, "row LUT allocation failed");
     return TG_OK;

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "fbm_params.h"
 #include "lattice.cuh"
@@ -462,7 +463,28 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             for (int c = 0; c < CH; ++c) grid[c * kGridCap + od.goff + cy * od.pitch + cx] = d[c];
         }
     }
-    // (b) everything else with a grid
+    // (b) aligned power-of-two grids, ppc = 1 .. 16: one slot per ppc with a
+    // compile-time shape (FineDev, built by the host planner)
+    auto fine_slot = [&](auto sh_c) {
+        constexpr int SH = decltype(sh_c)::value;
+        const FineDev& fd = args.fine[SH];
+        if ((TG_SKIP & 1) || fd.goff < 0) return;
+        const uint64_t p0 = seed_key + fd.key0 + static_cast<uint64_t>(blockIdx.x) * fd.kx +
+                            static_cast<uint64_t>(blockIdx.y) * fd.ky;
+        float* g = grid + fd.goff;
+        fine_grid<SH, CH>(g, fd.pitch, p0, warp, lane, tid, fd.rot, grid_value, args.oct[fd.oct]);
+    };
+    // (generic keeps its aligned grids in the list below: one runtime-shaped
+    // copy of the 3-lane corner hash, two lanes with sincos — five
+    // specialisations cost more than they save, 324 -> 398 us at config 3)
+    if constexpr (KIND != kGeneric) {
+        fine_slot(std::integral_constant<int, 0>{});
+        fine_slot(std::integral_constant<int, 1>{});
+        fine_slot(std::integral_constant<int, 2>{});
+        fine_slot(std::integral_constant<int, 3>{});
+        fine_slot(std::integral_constant<int, 4>{});
+    }
+    // (c) everything else with a grid
     for (int q = 0; q < TG_NG(kGProFine, 1); ++q) {
         const OctDev& od = args.oct[args.group[kGProFine][q]];
         const uint64_t base = seed_key + od.oct_key;
@@ -504,26 +526,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         }
         const int pitch = od.pitch;
         float* g = grid + od.goff;
-        if (aligned && od.shift <= 4) {
+        if (KIND == kGeneric && aligned && od.shift <= 4) {
             const uint64_t p0 = seed_key + od.key0 + static_cast<uint64_t>(blockIdx.x) * od.kx +
                                 static_cast<uint64_t>(blockIdx.y) * od.ky;
-            // (Wm + 1) x (Hm + 1) corners, Wm = 128/ppc, Hm = 64/ppc, shapes
-            // fixed at compile time per ppc.  The starting warp / thread
-            // rotates with the list position so the small grids (ppc 8, 16)
-            // and the edge lists of successive octaves land on different warps.
-            const int rot = q & 7;
-            if constexpr (KIND == kGeneric) {
-                // one runtime-shaped copy: five specialisations of the 3-lane
-                // corner hash (two with sincos) cost more than they save
-                // (measured 321 -> 417 us at config 3)
-                fine_grid_rt<CH>(od.shift, g, pitch, p0, warp, lane, tid, rot, grid_value, od);
-            } else switch (od.shift) {
-                case 0: fine_grid<0, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
-                case 1: fine_grid<1, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
-                case 2: fine_grid<2, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
-                case 3: fine_grid<3, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
-                default: fine_grid<4, CH>(g, pitch, p0, warp, lane, tid, rot, grid_value, od); break;
-            }
+            fine_grid_rt<CH>(od.shift, g, pitch, p0, warp, lane, tid, q & 7, grid_value, od);
         } else {
             // Any other shape: flat corner list, four hash chains per thread.
             const uint64_t p0 = pack_xy(base, ix0, iy0);

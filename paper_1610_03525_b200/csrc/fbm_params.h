@@ -97,6 +97,18 @@ enum OctGroup : int32_t {
     kNumGroups = 9
 };
 
+// Aligned power-of-two corner grids with ppc = 2^s <= 16, one slot per s
+// (distinct octaves never share a ppc): the kernel visits the five slots with
+// compile-time shapes and per-slot constants at fixed parameter offsets
+// (no per-octave list walk).  goff < 0: slot unused.
+struct FineDev {
+    uint64_t key0, kx, ky;  // as OctDev::key0 / kx / ky
+    int32_t goff, pitch;    // grid offset / row stride (floats)
+    int32_t rot;            // starting warp (list position & 7)
+    int32_t oct;            // octave index (corner data of Perlin / generic grids)
+};
+constexpr int kFineSlots = 5;
+
 struct FbmArgs {
     int64_t ox, oy;          // window origin, global pixels
     int64_t tile_x0, tile_y0;  // tile-grid origin (aligned to the tile size in global px)
@@ -120,6 +132,7 @@ struct FbmArgs {
     int8_t group[kNumGroups][kMaxOctaves];
     uint64_t seed_key[kMaxBatch];  // seed * K1 per map (lattice.hpp:47)
     OctDev oct[kMaxOctaves];
+    FineDev fine[kFineSlots];  // kGProFine octaves taken out of the list (see FineDev)
 };
 
 struct Fbm3Args {
