@@ -398,6 +398,9 @@ __device__ __forceinline__ void zg_cols(float (&acc)[kRPT][4], float (&cacc)[4],
 #ifndef TG_ZG_LEAN_MIN_BLOCKS
 #define TG_ZG_LEAN_MIN_BLOCKS 4
 #endif
+#ifndef TG_SUB_ROWS
+#define TG_SUB_ROWS 2  // lattice-point octaves: pixel rows hashed per step (1, 2 or 4)
+#endif
 #ifndef TG_TMA_STORE
 #define TG_TMA_STORE 1
 #endif
@@ -901,6 +904,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const float amp = od.amp * kMapScale;  // exact power-of-two rescale
             // key(gx, gy) = seed*K1 + oct*K2 + (gx*k + k/2)*K3 + (gy*k + k/2)*K4,
             // tile / thread offsets as 32-bit multiples of the per-launch steps
+#if TG_SUB_ROWS == 1
             uint64_t X[4];
             X[0] = static_cast<uint64_t>(blockIdx.x * kTW + c0) * od.kx;
 #pragma unroll
@@ -915,6 +919,30 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(amp, h[j], acc[r][j]);
                 Y = add64(Y, dY);
             }
+#else
+            // TG_SUB_ROWS rows per step: 4 * TG_SUB_ROWS independent hash
+            // chains (the 4-chain form stalls on the IMAD dependency latency)
+            const uint64_t kx = od.kx, ky = od.ky;
+            uint64_t K = seed_key + od.key0 + static_cast<uint64_t>(blockIdx.y * kTH + r0) * ky +
+                         static_cast<uint64_t>(blockIdx.x * kTW + c0) * kx;  // (row r0, column c0)
+#pragma unroll
+            for (int r = 0; r < kRPT; r += TG_SUB_ROWS) {
+                uint64_t p[4 * TG_SUB_ROWS];
+#pragma unroll
+                for (int i = 0; i < TG_SUB_ROWS; ++i) {
+                    p[4 * i] = i ? add64(p[4 * (i - 1)], ky) : K;
+#pragma unroll
+                    for (int j = 1; j < 4; ++j) p[4 * i + j] = add64(p[4 * i + j - 1], kx);
+                }
+                float h[4 * TG_SUB_ROWS];
+                map_heightN<4 * TG_SUB_ROWS>(p, h);
+#pragma unroll
+                for (int i = 0; i < TG_SUB_ROWS; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[r + i][j] = fmaf(amp, h[4 * i + j], acc[r + i][j]);
+                if (r + TG_SUB_ROWS < kRPT) K = add64(p[4 * (TG_SUB_ROWS - 1)], ky);
+            }
+#endif
         }
     }
 

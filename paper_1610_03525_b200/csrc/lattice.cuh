@@ -157,6 +157,29 @@ __device__ __forceinline__ void hash_top_word4(uint64_t p0, uint64_t p1, uint64_
             : "r"(l[i]), "r"(h[i]));
 }
 
+// N independent keys in lock step (N-way instruction-level parallelism).
+template <int N>
+__device__ __forceinline__ void hash_top_wordN(const uint64_t (&p)[N], uint32_t (&out)[N]) {
+    uint32_t l[N], h[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        l[i] = static_cast<uint32_t>(p[i]);
+        h[i] = static_cast<uint32_t>(p[i] >> 32);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) l[i] ^= h[i] >> 1;
+#pragma unroll
+    for (int i = 0; i < N; ++i) TG_MUL64(l[i], h[i], 0xED558CCD, 0xFF51AFD7);
+#pragma unroll
+    for (int i = 0; i < N; ++i) l[i] ^= h[i] >> 1;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
+            "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
+            : "=r"(out[i])
+            : "r"(l[i]), "r"(h[i]));
+}
+
 // The height representation of the map kernels: the corner height is
 // map_height(p) * kMapScale - kMapOffsetUnits (the second term folded into
 // FbmArgs::hoff = -sum(amp), scaled by kMapOffsetUnits in the kernels).
@@ -174,6 +197,13 @@ constexpr float kMapOffsetUnits = 1.0f;
 __device__ __forceinline__ float top_word_height(uint32_t t) { return static_cast<float>(t); }
 constexpr bool kMapOffset = true;
 __device__ __forceinline__ float map_height(uint64_t p) { return top_word_height(hash_top_word(p)); }
+template <int N>
+__device__ __forceinline__ void map_heightN(const uint64_t (&p)[N], float (&o)[N]) {
+    uint32_t t[N];
+    hash_top_wordN<N>(p, t);
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = top_word_height(t[i]);
+}
 __device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
     uint32_t t[4];
     hash_top_word4(p0, p1, p2, p3, t);
@@ -185,6 +215,11 @@ constexpr float kMapScale = 0x1p-63f;
 constexpr bool kMapOffset = false;
 constexpr float kMapOffsetUnits = 0.0f;
 __device__ __forceinline__ float map_height(uint64_t p) { return height_scaled(p); }
+template <int N>
+__device__ __forceinline__ void map_heightN(const uint64_t (&p)[N], float (&o)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = height_scaled(p[i]);
+}
 __device__ __forceinline__ void map_height4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, float (&o)[4]) {
     height_scaled4(p0, p1, p2, p3, o);
 }
