@@ -321,7 +321,11 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
             // ppc >= 32 on a 128 x 64 tile: at most 4 x 2 cells, 15 corners
             const bool tile_terms = paper && d.shift >= 5 && tg::fbm2d_tile_h() == 64 && d.ncx * d.ncy <= 32 &&
                                     a->ngroup[tg::kGBlkT] < tg::kMaxCellSlots;
-            if (tile_terms) a->oct[o].cslot = a->ngroup[tg::kGBlkT];
+            if (tile_terms) {
+                const int q = a->ngroup[tg::kGBlkT];
+                a->oct[o].cslot = q;
+                a->blkt[q] = {d.shift, d.ncx - 1, d.lut_off, d.inv_ppc};
+            }
             push(tile_terms ? tg::kGBlkT : tg::kGBlk8);
         }
         else if (zg && d.mode == tg::kModeBlock && d.shift == 2) push(tg::kGBlk4);

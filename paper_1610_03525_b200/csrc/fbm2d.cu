@@ -274,6 +274,8 @@ __device__ __forceinline__ void fine_grid(float* g, int pitch, uint64_t p0, int 
     const int wv = (warp - rot) & 7;
     const int cg = lane & ((1 << LSH) - 1), rs = lane >> LSH;
     const int cy0 = (wv << SH) + rs;
+    // ppc >= 4: only the first Hm >> SH warps hold main-block rows (warp-uniform skip)
+    if (Hm >= RSTEP || (wv << SH) < Hm) {
     uint64_t p = p0 + static_cast<uint64_t>(4 * cg) * kIxMul + static_cast<uint64_t>(static_cast<uint32_t>(cy0)) * kIyMul;
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
@@ -295,6 +297,7 @@ __device__ __forceinline__ void fine_grid(float* g, int pitch, uint64_t p0, int 
                     make_float4(d[0][c], d[1][c], d[2][c], d[3][c]);
         }
         if (it + 1 < NIT) p = add64(p, static_cast<uint64_t>(RSTEP) * kIyMul);
+    }
     }
     constexpr int NE = Hm + 1 + Wm;  // last column (Hm + 1 corners) then last row (Wm)
     for (int i = (tid - 32 * rot) & (kThreads - 1); i < NE; i += kThreads) {
@@ -596,42 +599,75 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 //   Cw = h00 + Sx*dx + (a*yc)*(Sx - x), C1 = (a/ppc)*(Sx - x),
                 //   Rw = Sy*(dy + a*xc),                R1 = (a/ppc)*Sy.
                 // Cells nest, so every octave's (cc, cr) follows from the
-                // ppc-32 cell: thread t builds the column entry (X = t % 128,
-                // ppc-32 cell row t / 128) and the row entry (Y = t % 64,
-                // ppc-32 cell column t / 64), summed over the whole list.
+                // ppc-32 cell; the entries are summed over the whole list.
                 float* feat = reinterpret_cast<float*>(smem_raw + smem_grid_end<KIND, LEAN>());
-                const int X = tid & 127, crP = tid >> 7, Y = tid & 63, ccP = tid >> 6;
-                float cw = 0.f, c1 = 0.f, rw = 0.f, r1 = 0.f;
+                // Threads 0-127 build the column entries of X = tid for both
+                // ppc-32 cell rows, threads 128-255 the row entries of
+                // Y = tid % 64 for two ppc-32 cell columns; above ppc 32 the
+                // two entries share their cell, so the term is computed once.
                 const float4* cpar = reinterpret_cast<const float4*>(feat) + 256;
-                for (int q = 0; q < args.ngroup[kGBlkT]; ++q) {
-                    const OctDev& od = args.oct[args.group[kGBlkT][q]];
-                    const int sh = od.shift, mask = od.ppc - 1, cw1 = od.ncx - 1;
-                    const float inv = od.inv_ppc;
-                    const int tmx = static_cast<int>(tx0 & mask), tmy = static_cast<int>(ty0 & mask);
-                    const float4* cq = cpar + od.cslot * 8;
-                    {  // column entry
-                        const int cx = X >> sh, cr = (crP << 5) >> sh;
-                        const float4 cp = cq[cr * cw1 + cx];  // h00, dx, dy, a
-                        const int mx = (tmx + X) & mask;
-                        const float sx = __ldg(lutS + od.ppc + mx), d = __ldg(lutD + od.ppc + mx);
-                        const float yc = (static_cast<float>(tmy - (cr << sh)) + 0.5f) * inv;
-                        cw += fmaf(cp.w * yc, d, fmaf(sx, cp.y, cp.x));
-                        c1 = fmaf(cp.w * inv, d, c1);
+                const int tlx = static_cast<int>(tx0), tly = static_cast<int>(ty0);  // (& mask: low bits)
+                const int nq = args.ngroup[kGBlkT];
+                if (tid < 128) {
+                    const int X = tid;
+                    float cwA = 0.f, cwB = 0.f, c1A = 0.f, c1B = 0.f;
+                    for (int q = 0; q < nq; ++q) {
+                        const BlkTDev b = args.blkt[q];
+                        const int sh = b.shift, mask = (1 << sh) - 1;
+                        const int tmy = tly & mask;
+                        const float4* cq = cpar + q * 8;
+                        const float4 e = __ldg(args.lut + b.lut_off + ((tlx + X) & mask));  // x, S, S - x
+                        const int cx = X >> sh;
+                        const float4 cp = cq[cx];  // h00, dx, dy, a
+                        const float yc = (static_cast<float>(tmy) + 0.5f) * b.inv;
+                        const float tA = fmaf(cp.w * yc, e.z, fmaf(e.y, cp.y, cp.x));
+                        const float uA = cp.w * b.inv;
+                        cwA += tA;
+                        c1A = fmaf(uA, e.z, c1A);
+                        if (sh == 5) {  // second ppc-32 cell row
+                            const float4 cpB = cq[b.ncx1 + cx];
+                            const float ycB = (static_cast<float>(tmy - 32) + 0.5f) * b.inv;
+                            cwB += fmaf(cpB.w * ycB, e.z, fmaf(e.y, cpB.y, cpB.x));
+                            c1B = fmaf(cpB.w * b.inv, e.z, c1B);
+                        } else {
+                            cwB += tA;
+                            c1B = fmaf(uA, e.z, c1B);
+                        }
                     }
-                    {  // row entry
-                        const int cc = (ccP << 5) >> sh, cr = Y >> sh;
-                        const float4 cp = cq[cr * cw1 + cc];
-                        const int my = (tmy + Y) & mask;
-                        const float sy = __ldg(lutS + od.ppc + my);
-                        const float xc = (static_cast<float>(tmx - (cc << sh)) + 0.5f) * inv;
-                        rw = fmaf(sy, fmaf(cp.w, xc, cp.z), rw);
-                        r1 = fmaf(cp.w * inv, sy, r1);
+                    feat[X] = cwA;
+                    feat[128 + X] = cwB;
+                    feat[256 + X] = c1A;
+                    feat[384 + X] = c1B;
+                } else {
+                    const int u = tid - 128, Y = u & 63, ccA = (u >> 6) * 2;
+                    float rwA = 0.f, rwB = 0.f, r1A = 0.f, r1B = 0.f;
+                    for (int q = 0; q < nq; ++q) {
+                        const BlkTDev b = args.blkt[q];
+                        const int sh = b.shift, mask = (1 << sh) - 1;
+                        const int tmx = tlx & mask;
+                        const float4* cq = cpar + q * 8;
+                        const float sy = __ldg(args.lut + b.lut_off + ((tly + Y) & mask)).y;
+                        const int cr = Y >> sh, cc = (ccA << 5) >> sh;
+                        const float4 cp = cq[cr * b.ncx1 + cc];
+                        const float xc = (static_cast<float>(tmx - (cc << sh)) + 0.5f) * b.inv;
+                        const float tA = fmaf(cp.w, xc, cp.z), uA = cp.w * b.inv;
+                        rwA = fmaf(sy, tA, rwA);
+                        r1A = fmaf(uA, sy, r1A);
+                        if (sh == 5) {  // second ppc-32 cell column
+                            const float4 cpB = cq[cr * b.ncx1 + cc + 1];
+                            const float xcB = (static_cast<float>(tmx - ((cc + 1) << sh)) + 0.5f) * b.inv;
+                            rwB = fmaf(sy, fmaf(cpB.w, xcB, cpB.z), rwB);
+                            r1B = fmaf(cpB.w * b.inv, sy, r1B);
+                        } else {
+                            rwB = fmaf(sy, tA, rwB);
+                            r1B = fmaf(uA, sy, r1B);
+                        }
                     }
+                    feat[512 + ccA * 64 + Y] = rwA;
+                    feat[512 + (ccA + 1) * 64 + Y] = rwB;
+                    feat[768 + ccA * 64 + Y] = r1A;
+                    feat[768 + (ccA + 1) * 64 + Y] = r1B;
                 }
-                feat[tid] = cw;
-                feat[256 + tid] = c1;
-                feat[512 + tid] = rw;
-                feat[768 + tid] = r1;
                 __syncthreads();
                 // the thread's block: X = c0 + j, Y = r0 + r (block-local c = j, r = r)
                 const float* fc = feat + (r0 >> 5) * 128 + c0;

@@ -109,6 +109,13 @@ struct FineDev {
 };
 constexpr int kFineSlots = 5;
 
+// kGBlkT octave q (ppc = 2^shift >= 32): per-slot constants of the per-tile
+// column / row terms, indexed by list position (cell parameters at slot q).
+struct BlkTDev {
+    int32_t shift, ncx1, lut_off;  // log2 ppc, cell columns per tile (ncx - 1), row LUT offset
+    float inv;                     // 1 / ppc
+};
+
 struct FbmArgs {
     int64_t ox, oy;          // window origin, global pixels
     int64_t tile_x0, tile_y0;  // tile-grid origin (aligned to the tile size in global px)
@@ -133,6 +140,7 @@ struct FbmArgs {
     uint64_t seed_key[kMaxBatch];  // seed * K1 per map (lattice.hpp:47)
     OctDev oct[kMaxOctaves];
     FineDev fine[kFineSlots];  // kGProFine octaves taken out of the list (see FineDev)
+    BlkTDev blkt[kMaxCellSlots];
 };
 
 struct Fbm3Args {
