@@ -187,6 +187,7 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
         d.ncy = static_cast<int32_t>(ncy);
         d.pitch = static_cast<int32_t>(pitch);
         d.goff = goff;
+        d.cdiv = static_cast<int32_t>((65536 + ncx - 1) / ncx);
         goff += static_cast<int>(size);
         if (needs_tab) d.tslot = slot++;
     }

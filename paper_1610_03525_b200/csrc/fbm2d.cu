@@ -448,7 +448,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     // (a) coarse aligned octaves (<= 32 corners): one warp per octave.
     for (int q = warp; q < args.ngroup[kGProCoarse]; q += kThreads / 32) {
         const OctDev& od = args.oct[args.group[kGProCoarse][q]];
-        const int cy = lane / od.ncx, cx = lane - cy * od.ncx;
+        const int cy = (lane * od.cdiv) >> 16, cx = lane - cy * od.ncx;  // lane / ncx (lane < 32, ncx <= 32)
         if (KIND == kZgPaper && kRPT == 8 && od.cslot >= 0) {
             // kGBlkT octave: the cells' (h00, dx, dy, a) x amp straight from
             // the lanes' corners (lane = cy * ncx + cx), no grid
@@ -475,6 +475,12 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         constexpr int SH = decltype(sh_c)::value;
         const FineDev& fd = args.fine[SH];
         if ((TG_SKIP & 1) || fd.goff < 0) return;
+        // ppc >= 4: main block and edge list both sit on the first few warps
+        // from fd.rot (rot == erot), the others skip the slot outright
+        constexpr int Hm = kTH >> SH, NE = Hm + 1 + (kTW >> SH);
+        constexpr int kMainW = Hm >= (8 << SH) ? 8 : (Hm + (1 << SH) - 1) >> SH;
+        constexpr int kActW = kMainW > (NE + 31) / 32 ? kMainW : (NE + 31) / 32;
+        if (kActW < 8 && ((warp - fd.rot) & 7) >= kActW) return;
         const uint64_t p0 = seed_key + fd.key0 + static_cast<uint64_t>(blockIdx.x) * fd.kx +
                             static_cast<uint64_t>(blockIdx.y) * fd.ky;
         float* g = grid + fd.goff;

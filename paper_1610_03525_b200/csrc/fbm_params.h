@@ -69,7 +69,7 @@ struct OctDev {
     int32_t lut_off;   // offset of this ppc's row LUT (aligned modes) or -1
     int32_t pad;       // 3D: corner grid depth (ncz)
     int32_t cslot;     // kGBlkT: slot of the octave's per-tile cell parameters, else -1
-    int32_t pad2;
+    int32_t cdiv;      // 2D coarse grids: ceil(2^16 / ncx), so lane / ncx = (lane * cdiv) >> 16 for lane < 32
     // per-launch lattice-key constants (2D, build_args): the packed key of a
     // tile's first corner / lattice point is seed*K1 + key0 + bx*kx + by*ky
     //   lattice-point octaves: key0 = oct*K2 + (tile_x0*k + k/2)*K3 + (tile_y0*k + k/2)*K4,
