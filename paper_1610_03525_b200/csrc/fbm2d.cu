@@ -237,6 +237,25 @@ constexpr size_t smem_bytes() {
     return smem_grid_end<KIND, LEAN>() + (KIND == kZgPaper ? sizeof(float) * kFeat : 0);
 }
 
+// Corner weights of a zero-gradient cell at ppc = 2 (kernels2d.hpp:62-76):
+// position (ix, iy) has x = (2 ix + 1)/4, y = (2 iy + 1)/4; corner k = 0..3 is
+// h00, h10, h01, h11.  paper: c = Sx*y + Sy*x - x*y; separable: c = Sx*Sy;
+// w = (1 - Sx - Sy + c, Sx - c, Sy - c, c).  Every term is exact in fp32.
+template <int KIND, int ORDER>
+struct Ppc2W {
+    static constexpr float S(int i) {  // S(1/4), S(3/4) (smoothstep3/5, kernels2d.hpp:26-38)
+        return ORDER == 5 ? (i ? 0.896484375f : 0.103515625f) : (i ? 0.84375f : 0.15625f);
+    }
+    static constexpr float X(int i) { return i ? 0.75f : 0.25f; }
+    static constexpr float C(int ix, int iy) {
+        return KIND == kZgSeparable ? S(ix) * S(iy) : S(ix) * X(iy) + S(iy) * X(ix) - X(ix) * X(iy);
+    }
+    static constexpr float w(int ix, int iy, int k) {
+        return k == 0 ? 1.0f - S(ix) - S(iy) + C(ix, iy)
+                      : k == 1 ? S(ix) - C(ix, iy) : k == 2 ? S(iy) - C(ix, iy) : C(ix, iy);
+    }
+};
+
 // q*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
 // rows r = 0..8 of a 5-wide corner strip: x = y = 0.5 makes every zero-
 // gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners
@@ -400,6 +419,9 @@ __device__ __forceinline__ void zg_cols(float (&acc)[kRPT][4], float (&cacc)[4],
 #endif
 #ifndef TG_ZG_LEAN_MIN_BLOCKS
 #define TG_ZG_LEAN_MIN_BLOCKS 4
+#endif
+#ifndef TG_PPC2_WEIGHTS
+#define TG_PPC2_WEIGHTS 1  // zero-gradient ppc-2 octaves as fixed corner blends
 #endif
 #ifndef TG_SUB_ROWS
 #define TG_SUB_ROWS 2  // lattice-point octaves: pixel rows hashed per step (1, 2 or 4)
@@ -850,7 +872,47 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
 
     // ppc == 2: columns (0,1) | (2,3) are two cells at x = 0.25, 0.75; rows
     // pair up the same way; 3 corners per corner row.
+#if TG_PPC2_WEIGHTS
+    // Zero-gradient kinds: every pixel sits at one of the 4 cell positions
+    // (x, y) in {1/4, 3/4}^2, so it is a fixed blend of its 4 corners,
+    //   v = w00*h00 + w10*h10 + w01*h01 + w11*h11,
+    // with compile-time weights (S(1/4), S(3/4) and x*y exact in fp32):
+    // 4 FFMA per pixel from the (amp-scaled) corners, no per-cell set-up.
+    if constexpr (kZg) {
+        for (int q = 0; q < TG_NG(kGBlk2, 32); ++q) {
+            const OctDev& od = args.oct[args.group[kGBlk2][q]];
+            const int pitch = od.pitch;
+            const float sc = od.amp * kMapScale;
+            const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
+            float t[3];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) t[u] = sc * g[u];
+#pragma unroll
+            for (int k = 0; k < kRPT / 2; ++k) {
+                const float* gn = g + (k + 1) * pitch;
+                float b[3];
+#pragma unroll
+                for (int u = 0; u < 3; ++u) b[u] = sc * gn[u];
+#pragma unroll
+                for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int cc = j >> 1, ix = j & 1;
+                        float& a = acc[2 * k + iy][j];
+                        a = fmaf(Ppc2W<KIND, ORDER>::w(ix, iy, 3), b[cc + 1], a);
+                        a = fmaf(Ppc2W<KIND, ORDER>::w(ix, iy, 2), b[cc], a);
+                        a = fmaf(Ppc2W<KIND, ORDER>::w(ix, iy, 1), t[cc + 1], a);
+                        a = fmaf(Ppc2W<KIND, ORDER>::w(ix, iy, 0), t[cc], a);
+                    }
+#pragma unroll
+                for (int u = 0; u < 3; ++u) t[u] = b[u];
+            }
+        }
+    }
+    for (int q = 0; q < (kZg ? 0 : TG_NG(kGBlk2, 32)); ++q) {
+#else
     for (int q = 0; q < TG_NG(kGBlk2, 32); ++q) {
+#endif
         const OctDev& od = args.oct[args.group[kGBlk2][q]];
         const float4 e0 = args.lut[od.lut_off], e1 = args.lut[od.lut_off + 1];
         const int pitch = od.pitch;
