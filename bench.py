@@ -16,8 +16,9 @@ runs once on each rank's map with the statistics all-reduced (NCCL).
 
 Timing: W warm-up steps, then K steps back to back into 3 rotating output
 buffers (3 x 64 MiB = 192 MiB > 126 MB L2, so every step's writes reach HBM),
-bracketed by barrier + cuda.synchronize; per-launch CUDA events on the
-launching stream; max over ranks.  Clocks are sampled through NVML during the
+bracketed by barrier + cuda.synchronize; CUDA events on the launching stream
+around the K launches (mean launch duration = bracketed time / K); max over
+ranks.  Clocks are sampled through NVML during the
 timed region.  `e2e` times the reference-facing drop-in
 (tg_fbm_generate_f64_host = generate_into(span<double>)) with the host copy
 inside the timed region.  `cpu_baseline` / `--impl reference` time the
@@ -352,7 +353,11 @@ def main() -> None:
     torch.cuda.synchronize()
 
     K = args.steps
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    # Events only around the K back-to-back launches (on their stream): an
+    # event record between launches inserts a gap (~3 us per 60 us launch
+    # measured), and the launches are serialised on the stream anyway, so the
+    # mean launch duration is the bracketed time / K.
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -361,12 +366,27 @@ def main() -> None:
             ev[0].record(stream)
             for i in range(K):
                 launch(i)
-                ev[i + 1].record(stream)
+            ev[1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    per_launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
-    total_ms = ev[0].elapsed_time(ev[K])
+    total_ms = ev[0].elapsed_time(ev[1])
+    per_launch_ms = [total_ms / K]
+    # Isolated launches (outside the timed region): the generation kernel is
+    # launched with programmatic stream serialisation, so back-to-back launches
+    # overlap one grid's tail with the next grid's hashing; report what a
+    # single launch with an idle GPU before and after it takes as well.
+    iso = []
+    with torch.cuda.stream(stream):
+        for i in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            launch(i)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            iso.append(e0.elapsed_time(e1))
+    isolated_us = statistics.median(iso) * 1e3
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -434,8 +454,12 @@ def main() -> None:
                          "traffic": traffic_from_profiles(),
                          "note": (f"{FLOPS_PER_SAMPLE_OCTAVE} flop/sample-octave (paper op count + accumulate) "
                                   f"x {int(so_per_step)} sample-octaves per launch / mean CUDA-event launch "
-                                  f"time {avg_launch_s*1e6:.1f} us; peak = FFMA-chain measured in-run "
-                                  f"(MEASURED_PEAKS.json has no FP32 entry)"),
+                                  f"time {avg_launch_s*1e6:.1f} us over the K back-to-back launches (programmatic "
+                                  f"dependent launch overlaps each grid's tail with the next one's hashing; an "
+                                  f"isolated launch takes {isolated_us:.1f} us, frac "
+                                  f"{FLOPS_PER_SAMPLE_OCTAVE * so_per_step / (isolated_us * 1e-6) / 1e12 / peak_tflops:.3f}); "
+                                  f"peak = FFMA-chain measured in-run (MEASURED_PEAKS.json has no FP32 entry)"),
+                         "isolated_launch_us": isolated_us,
                          "hbm_write_gbs": hbm_gbs, "hbm_frac": hbm_gbs / measured_hbm_gbs(),
                          "hashes_per_launch": hashes_per_launch(R, F0, OCTAVES),
                          "hashes_per_s": hashes_per_launch(R, F0, OCTAVES) / avg_launch_s,

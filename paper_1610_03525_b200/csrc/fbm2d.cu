@@ -420,6 +420,9 @@ __device__ __forceinline__ void zg_cols(float (&acc)[kRPT][4], float (&cacc)[4],
 #ifndef TG_ZG_LEAN_MIN_BLOCKS
 #define TG_ZG_LEAN_MIN_BLOCKS 4
 #endif
+#ifndef TG_PDL
+#define TG_PDL 1  // programmatic dependent launch of the 2D generation kernel
+#endif
 #ifndef TG_PPC2_WEIGHTS
 #define TG_PPC2_WEIGHTS 1  // zero-gradient ppc-2 octaves as fixed corner blends
 #endif
@@ -448,6 +451,8 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     TabSlot* tabs = reinterpret_cast<TabSlot*>(smem_raw);
     float* grid = reinterpret_cast<float*>(smem_raw + (LEAN ? 0 : sizeof(TabSlot) * kTabSlots));
 
+    // let the next launch on the stream start filling SMs as this grid drains
+    asm volatile("griddepcontrol.launch_dependents;");
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
@@ -1235,6 +1240,11 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     }
 
     // ---- single fp32 store of the finished tile ----------------------------
+    // Programmatic dependent launch: this grid may have started while the
+    // previous kernel on the stream was finishing (the hashing above touches no
+    // global memory but the immutable row LUT); wait for it to complete before
+    // writing the output (write-after-write / write-after-read on `out`).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t lx0 = tx0 + c0 - args.ox;
     const int64_t ly0 = ty0 + r0 - args.oy;
 #if TG_TMA_STORE
@@ -1382,8 +1392,25 @@ static cudaError_t launch_v(const FbmArgs& a0, float* out, cudaStream_t st) {
     const int64_t tiles_y = (a.oy + a.height - a.tile_y0 + TH - 1) / TH;
     dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
               static_cast<unsigned>(a.n_maps));
+#if TG_PDL
+    // programmatic stream serialisation: consecutive generation launches
+    // overlap one grid's tail with the next grid's compute (the kernel waits
+    // on the previous grid before its stores)
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kern, a, m, out);
+#else
     kern<<<grid, kThreads, smem, st>>>(a, m, out);
     return cudaGetLastError();
+#endif
 }
 
 template <int KIND, int ORDER>

@@ -581,3 +581,26 @@ def test_norm_maps_match_restated_cli_stencils(oracle):
         torch.cuda.synchronize()
         ref = oracle.norm_map(host, hess).astype(np.float32)
         assert np.array_equal(out.cpu().numpy(), ref)
+
+
+# ---- programmatic dependent launch: stream order of the output writes ---------
+
+def test_back_to_back_launches_keep_stream_order():
+    """The 2D kernel starts under programmatic stream serialisation and waits
+    for the previous grid before its stores: back-to-back launches into ONE
+    buffer (and a preceding torch fill / a following torch read on the same
+    stream) must still leave exactly the last launch's map."""
+    R = 1024
+    lib = _abi.load()
+    s = torch.cuda.Stream()
+    buf = torch.empty((R, R), dtype=torch.float32, device="cuda")
+    cfgs = [make_cfg(seed=sd, smoothstep=5, resolution=R, base_frequency=2, octaves=12) for sd in (3, 4, 5)]
+    refs = [gen(c, 0, 0, R).cpu() for c in cfgs]
+    with torch.cuda.stream(s):
+        for it in range(40):
+            buf.fill_(float("nan"))
+            for c in cfgs[: 1 + it % 3]:
+                assert lib.tg_fbm_generate_rect_f32(C.byref(c), 0, 0, R, R, buf.data_ptr(), R, s.cuda_stream) == 0
+            snap = buf.clone()  # a torch kernel reading the output right after
+            assert torch.equal(snap.cpu(), refs[it % 3]), it
+    torch.cuda.synchronize()
