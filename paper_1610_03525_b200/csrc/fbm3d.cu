@@ -171,25 +171,29 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         const int pitch = od.pitch, plane = pitch * od.ncy;  // strides use the planned bounds
         float* g = grid3 + od.goff;
         const int nrows = ncy * ncz;
-        if (od.lut_off >= 0 && od.shift == 0) {
-            // ppc = 1: 129 x 9 x 9 corners; 4 consecutive x per lane (four hash
-            // chains, one 16-byte store), the last column through a flat loop.
-            const uint64_t px = p0 + static_cast<uint64_t>(4 * lane) * kIxMul;
-            for (int rw = warp; rw < nrows; rw += kThreads3 / 32) {
-                const int cz = rw / ncy, cy = rw - cz * ncy;
-                const uint64_t p = px + static_cast<uint64_t>(cy) * kIyMul + static_cast<uint64_t>(cz) * kIzMul;
-                float4 v;
-                v.x = map_height(p);
-                v.y = map_height(add64(p, kIxMul));
-                v.z = map_height(add64(p, 2 * kIxMul));
-                v.w = map_height(add64(p, 3 * kIxMul));
-                *reinterpret_cast<float4*>(g + cz * plane + cy * pitch + 4 * lane) = v;
+        if (od.lut_off >= 0 && od.shift <= 5) {
+            // aligned power-of-two grid, Wm = 128 >> s >= 4 corner columns
+            // before the last: 4 consecutive x per lane (four hash chains, one
+            // 16-byte store), 2^s corner rows (cy, cz) per warp pass; the last
+            // column through a flat loop.  rw / ncy by a multiplier (rw < 2^7).
+            const int sh = od.shift, lsh = 5 - sh, Wm = kTX >> sh;
+            const int cg = lane & ((1 << lsh) - 1), rsub = lane >> lsh, rpw = 1 << sh;
+            const int cdiv = (65536 + ncy - 1) / ncy;
+            const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
+            for (int rw = warp * rpw + rsub; rw < nrows; rw += (kThreads3 / 32) * rpw) {
+                const int cz = (rw * cdiv) >> 16, cy = rw - cz * ncy;
+                const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul +
+                                   static_cast<uint64_t>(static_cast<uint32_t>(cz)) * kIzMul;
+                float h[4];
+                map_height4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
+                *reinterpret_cast<float4*>(g + cz * plane + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
             }
             for (int rw = tid; rw < nrows; rw += kThreads3) {
-                const int cz = rw / ncy, cy = rw - cz * ncy;
-                g[cz * plane + cy * pitch + kTX] =
-                    map_height(p0 + static_cast<uint64_t>(kTX) * kIxMul + static_cast<uint64_t>(cy) * kIyMul +
-                                  static_cast<uint64_t>(cz) * kIzMul);
+                const int cz = (rw * cdiv) >> 16, cy = rw - cz * ncy;
+                g[cz * plane + cy * pitch + Wm] =
+                    map_height(p0 + static_cast<uint64_t>(static_cast<uint32_t>(Wm)) * kIxMul +
+                               static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul +
+                               static_cast<uint64_t>(static_cast<uint32_t>(cz)) * kIzMul);
             }
         } else {
             const int n = ncx * nrows;
@@ -280,40 +284,63 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         if (mode == kM3Blk) {  // power-of-two ppc >= 2 on the aligned tile grid
             const int sh = od.shift, mask = od.ppc - 1;
             const float4* L = a.lut + od.lut_off;
+            // planar S(x) copy of the row LUT: S at float [ppc + r] (kernels.cu row_lut)
+            const float* LS = reinterpret_cast<const float*>(a.lut + kLutN4) + od.ppc;
             const int xo = static_cast<int>(tx0 & mask) + c0;
             const int yo = static_cast<int>(ty0 & mask) + warp;
             const int zo = static_cast<int>(tz0 & mask);
             const float sy = L[yo & mask].y;
             float sx[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) sx[j] = L[(xo + j) & mask].y;
+            if (sh >= 2) {  // xo % 4 == 0 and ppc >= 4: 4 consecutive entries
+                const float4 v = __ldg(reinterpret_cast<const float4*>(LS + (xo & mask)));
+                sx[0] = v.x;
+                sx[1] = v.y;
+                sx[2] = v.z;
+                sx[3] = v.w;
+            } else {  // ppc = 2: x = 1/4, 3/4 alternate
+                sx[0] = sx[2] = LS[0];
+                sx[1] = sx[3] = LS[1];
+            }
             const float* gy = grid3 + od.goff + (yo >> sh) * pitch;
             if (sh >= 2) {
-                // the thread's 4 columns share one x-cell; B0 -> per-slice accumulator
+                // the thread's 4 columns share one x-cell; B0 -> per-slice accumulator.
+                // ppc >= 8: the 8 slices lie in one z-cell (zo % 8 == 0), S(z)
+                // at 8 consecutive entries; ppc = 4: two z-cells, S(z & 3).
                 const float* g = gy + (xo >> sh);
-                int last = -1;
-                float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+                float szv[kTZ];
+                if (sh >= 3) {
+                    const float4 s0 = __ldg(reinterpret_cast<const float4*>(LS + zo));
+                    const float4 s1 = __ldg(reinterpret_cast<const float4*>(LS + zo + 4));
+                    szv[0] = s0.x; szv[1] = s0.y; szv[2] = s0.z; szv[3] = s0.w;
+                    szv[4] = s1.x; szv[5] = s1.y; szv[6] = s1.z; szv[7] = s1.w;
+                } else {
+                    const float4 s0 = __ldg(reinterpret_cast<const float4*>(LS));
+                    szv[0] = szv[4] = s0.x; szv[1] = szv[5] = s0.y; szv[2] = szv[6] = s0.z; szv[3] = szv[7] = s0.w;
+                }
 #pragma unroll
-                for (int z = 0; z < kTZ; ++z) {
-                    const int zr = zo + z, cz = zr >> sh;
-                    if (cz != last) {
-                        const float* q = g + cz * plane;
-                        // y-lerps of the x=0 / x=1 edges at z = cz, cz+1
-                        e0 = amp * lerp(q[0], q[pitch], sy);
-                        e1 = amp * lerp(q[plane], q[plane + pitch], sy);
-                        e2 = amp * lerp(q[1], q[pitch + 1], sy);
-                        e3 = amp * lerp(q[plane + 1], q[plane + pitch + 1], sy);
-                        last = cz;
+                for (int zc = 0; zc < 2; ++zc) {
+                    if (zc == 1 && sh >= 3) break;  // one z-cell
+                    const float* q = g + ((zo >> sh) + zc) * plane;
+                    // y-lerps of the x=0 / x=1 edges at z = cz, cz+1
+                    const float e0 = amp * lerp(q[0], q[pitch], sy);
+                    const float e1 = amp * lerp(q[plane], q[plane + pitch], sy);
+                    const float e2 = amp * lerp(q[1], q[pitch + 1], sy);
+                    const float e3 = amp * lerp(q[plane + 1], q[plane + pitch + 1], sy);
+                    const int z0 = sh >= 3 ? 0 : 4 * zc, z1 = sh >= 3 ? kTZ : 4 * zc + 4;
+#pragma unroll
+                    for (int z = 0; z < kTZ; ++z) {
+                        if (z < z0 || z >= z1) continue;
+                        const float sz = szv[z];
+                        const float b0 = lerp(e0, e1, sz), d = lerp(e2, e3, sz) - b0;
+                        racc[z] += b0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(sx[j], d, acc[z][j]);
                     }
-                    const float sz = L[zr & mask].y;
-                    const float b0 = lerp(e0, e1, sz), d = lerp(e2, e3, sz) - b0;
-                    racc[z] += b0;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(sx[j], d, acc[z][j]);
                 }
             } else {
                 // ppc = 2: columns (0,1) and (2,3) are two x-cells
                 const float* g = gy + (xo >> 1);
+                const float sz0 = LS[0], sz1 = LS[1];
 #pragma unroll
                 for (int zc = 0; zc < kTZ / 2; ++zc) {
                     const float* q = g + ((zo >> 1) + zc) * plane;
@@ -326,7 +353,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
 #pragma unroll
                     for (int zz = 0; zz < 2; ++zz) {
                         const int z = 2 * zc + zz;
-                        const float sz = L[(zo + z) & mask].y;
+                        const float sz = zz ? sz1 : sz0;
                         const float b0 = lerp(e[0][0], e[0][1], sz);
                         const float b1 = lerp(e[1][0], e[1][1], sz);
                         const float b2 = lerp(e[2][0], e[2][1], sz);
@@ -403,18 +430,28 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
             }
         }
     }
-    // store (x fastest)
+    // store (x fastest): one 16-byte store per slice when the thread's 4
+    // voxels are inside the window and aligned, else per voxel
     const int64_t ly = ty0 + warp - a.oy;
     if (ly < 0 || ly >= a.ny) return;
+    const int64_t lx0 = tx0 + c0 - a.ox;
+    const bool vec = lx0 >= 0 && lx0 + 4 <= a.nx && ((lx0 | a.nx) & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    float* row = out + ((tz0 - a.oz) * a.ny + ly) * a.nx;
+    const int64_t zstride = a.ny * a.nx;
 #pragma unroll
-    for (int z = 0; z < kTZ; ++z) {
+    for (int z = 0; z < kTZ; ++z, row += zstride) {
         const int64_t lz = tz0 + z - a.oz;
         if (lz < 0 || lz >= a.nz) continue;
-        float* row = out + (lz * a.ny + ly) * a.nx;
+        if (vec) {
+            *reinterpret_cast<float4*>(row + lx0) =
+                make_float4(acc[z][0] + racc[z], acc[z][1] + racc[z], acc[z][2] + racc[z], acc[z][3] + racc[z]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t lx = tx0 + c0 + j - a.ox;
-            if (lx >= 0 && lx < a.nx) row[lx] = acc[z][j] + racc[z];
+            for (int j = 0; j < 4; ++j) {
+                const int64_t lx = lx0 + j;
+                if (lx >= 0 && lx < a.nx) row[lx] = acc[z][j] + racc[z];
+            }
         }
     }
 }

@@ -37,5 +37,10 @@ for name in ("cfg1", "cfg2", "cfg2sep", "cfg3p", "cfg3g", "cfg5"):
     buf = torch.empty((h, w), dtype=torch.float32, device="cuda")
     pt.generate_rect_device(pt.FbmConfig(**kw), (0, 0), w, h, buf)
     out[name] = buf.cpu().numpy()
+c4 = pt.FbmConfig(seed=1, method=pt.Method.zg_separable, resolution=512, base_frequency=8, octaves=8)
+for name, org, ext in (("cfg4", (0, 0, 0), (256, 256, 256)), ("cfg4odd", (64, 0, 128), (40, 72, 100))):
+    v = torch.empty(ext, dtype=torch.float32, device="cuda")  # (nz, ny, nx)
+    pt.generate3d_device(c4, org, ext, v)
+    out[name] = v.cpu().numpy()
 np.savez(f"/tmp/tg_maps_{sys.argv[2]}.npz", **out)
 print("dumped", sys.argv[2])
