@@ -116,6 +116,16 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
     const int64_t tz0 = a.tile_z0 + static_cast<int64_t>(blockIdx.z) * kTZ;
     const int c0 = lane * 4;
 
+    // Packed key of every aligned octave's first tile corner, one octave per
+    // lane (64-bit index products once per warp instead of once per thread),
+    // read back by shuffle in the prologue.
+    uint64_t lane_p0 = 0;
+    if (lane < a.octaves) {
+        const OctDev& od = a.oct[lane];
+        if (od.lut_off >= 0)
+            lane_p0 = pack3(a.seed_key + od.oct_key, tx0 >> od.shift, ty0 >> od.shift, tz0 >> od.shift);
+    }
+
     // ---- prologue: all octaves' tile corners (raw map_height values) ------
     for (int o = 0; o < a.octaves; ++o) {
         const OctDev& od = a.oct[o];
@@ -167,7 +177,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 tb.zs[r] = smooth3<ORDER>(z);
             }
         }
-        const uint64_t p0 = pack3(base, ix0, iy0, iz0);
+        const uint64_t p0 = od.lut_off >= 0 ? __shfl_sync(0xffffffffu, lane_p0, o) : pack3(base, ix0, iy0, iz0);
         const int pitch = od.pitch, plane = pitch * od.ncy;  // strides use the planned bounds
         float* g = grid3 + od.goff;
         const int nrows = ncy * ncz;
@@ -178,7 +188,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
             // column through a flat loop.  rw / ncy by a multiplier (rw < 2^7).
             const int sh = od.shift, lsh = 5 - sh, Wm = kTX >> sh;
             const int cg = lane & ((1 << lsh) - 1), rsub = lane >> lsh, rpw = 1 << sh;
-            const int cdiv = (65536 + ncy - 1) / ncy;
+            const int cdiv = od.cdiv;
             const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
             for (int rw = warp * rpw + rsub; rw < nrows; rw += (kThreads3 / 32) * rpw) {
                 const int cz = (rw * cdiv) >> 16, cy = rw - cz * ncy;
@@ -235,18 +245,30 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         const int pitch = od.pitch, plane = od.pitch * od.ncy;
 
         if (mode == kM3Sub) {  // lattice points: v = h(ix, iy, iz)
-            const int64_t k = od.k, half = od.k >> 1;
-            const uint64_t Y = base + static_cast<uint64_t>((ty0 + warp) * k + half) * kIyMul;
-            uint64_t X[4];
+            // host key constants (fbm3d_plan); two slices per step = 8
+            // independent hash chains
+            const uint64_t kx = od.kx, kz = od.kz;
+            uint64_t K = a.seed_key + od.key0 + static_cast<uint64_t>(blockIdx.x * kTX + c0) * kx +
+                         static_cast<uint64_t>(blockIdx.y * kTY + warp) * od.ky +
+                         static_cast<uint64_t>(blockIdx.z * kTZ) * kz;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) X[j] = add64(Y, static_cast<uint64_t>((tx0 + c0 + j) * k + half) * kIxMul);
-            uint64_t Z = static_cast<uint64_t>(tz0 * k + half) * kIzMul;
-            const uint64_t dZ = static_cast<uint64_t>(k) * kIzMul;
+            for (int z = 0; z < kTZ; z += 2) {
+                uint64_t p[8];
+                p[0] = K;
+                p[4] = add64(K, kz);
 #pragma unroll
-            for (int z = 0; z < kTZ; ++z) {
+                for (int j = 1; j < 4; ++j) {
+                    p[j] = add64(p[j - 1], kx);
+                    p[4 + j] = add64(p[3 + j], kx);
+                }
+                float h[8];
+                map_heightN<8>(p, h);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(amp, map_height(add64(X[j], Z)), acc[z][j]);
-                Z = add64(Z, dZ);
+                for (int j = 0; j < 4; ++j) {
+                    acc[z][j] = fmaf(amp, h[j], acc[z][j]);
+                    acc[z + 1][j] = fmaf(amp, h[4 + j], acc[z + 1][j]);
+                }
+                if (z + 2 < kTZ) K = add64(p[4], kz);
             }
             continue;
         }
@@ -496,7 +518,16 @@ void fbm3d_plan(Fbm3Args* a, int zg_sep_only) {
         d.tslot = -1;
         d.lut_off = -1;
         if (d.cls == kClsSubInt) {
+            // key(x, y, z) = seed*K1 + key0 + (bx*128 + c)*kx + (by*8 + w)*ky + (bz*8 + z)*kz
+            // with u = g*k + k/2 on every axis (lattice.hpp:46-50 + the 3D term)
             d.mode = kM3Sub;
+            const uint64_t k = static_cast<uint64_t>(d.k), h = k >> 1;
+            d.kx = k * kIxMul;
+            d.ky = k * kIyMul;
+            d.kz = k * kIzMul;
+            d.key0 = d.oct_key + (static_cast<uint64_t>(a->tile_x0) * k + h) * kIxMul +
+                     (static_cast<uint64_t>(a->tile_y0) * k + h) * kIyMul +
+                     (static_cast<uint64_t>(a->tile_z0) * k + h) * kIzMul;
             continue;
         }
         int64_t nx, ny, nz;
@@ -537,6 +568,7 @@ void fbm3d_plan(Fbm3Args* a, int zg_sep_only) {
         d.pad = static_cast<int32_t>(nz);
         d.pitch = static_cast<int32_t>(pitch);
         d.goff = goff;
+        d.cdiv = static_cast<int32_t>((65536 + ny - 1) / ny);  // row / ncy for rows < 2^7 (prologue)
         goff += static_cast<int>(size);
         if (mode == kM3Gen) d.tslot = slot++;
     }

@@ -77,6 +77,7 @@ struct OctDev {
     //   aligned ppc <= 16:     key0 = oct*K2 + (tile_x0 >> s)*K3 + (tile_y0 >> s)*K4,
     //                          kx = (128 >> s)*K3 (per tile), ky = (64 >> s)*K4 (per tile)
     uint64_t key0, kx, ky;
+    uint64_t kz;       // 3D lattice-point octaves: k*K5 per voxel slice (fbm3d_plan)
     double ratio;      // freq / R (OpenSimplex sample spacing), set by its launcher
 };
 
