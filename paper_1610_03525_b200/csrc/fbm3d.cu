@@ -134,7 +134,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
         const uint64_t base = a.seed_key + od.oct_key;
         int64_t ix0, iy0, iz0;
         int ncx = od.ncx, ncy = od.ncy, ncz = od.pad;
-        if (od.lut_off >= 0) {
+        if (LEAN || od.lut_off >= 0) {  // lean plans hold aligned grids only (launch3)
             ix0 = tx0 >> od.shift;
             iy0 = ty0 >> od.shift;
             iz0 = tz0 >> od.shift;
@@ -177,20 +177,24 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 tb.zs[r] = smooth3<ORDER>(z);
             }
         }
-        const uint64_t p0 = od.lut_off >= 0 ? __shfl_sync(0xffffffffu, lane_p0, o) : pack3(base, ix0, iy0, iz0);
+        const uint64_t p0 =
+            (LEAN || od.lut_off >= 0) ? __shfl_sync(0xffffffffu, lane_p0, o) : pack3(base, ix0, iy0, iz0);
         const int pitch = od.pitch, plane = pitch * od.ncy;  // strides use the planned bounds
         float* g = grid3 + od.goff;
         const int nrows = ncy * ncz;
-        if (od.lut_off >= 0 && od.shift <= 5) {
+        if ((LEAN || od.lut_off >= 0) && od.shift <= 5) {
             // aligned power-of-two grid, Wm = 128 >> s >= 4 corner columns
             // before the last: 4 consecutive x per lane (four hash chains, one
             // 16-byte store), 2^s corner rows (cy, cz) per warp pass; the last
             // column through a flat loop.  rw / ncy by a multiplier (rw < 2^7).
+            // starting warp / thread rotated per octave (the row counts do
+            // not divide evenly over the 8 warps)
+            const int wv = (warp - o) & 7, tv = (tid - 32 * o) & (kThreads3 - 1);
             const int sh = od.shift, lsh = 5 - sh, Wm = kTX >> sh;
             const int cg = lane & ((1 << lsh) - 1), rsub = lane >> lsh, rpw = 1 << sh;
             const int cdiv = od.cdiv;
             const uint64_t px = p0 + static_cast<uint64_t>(4 * cg) * kIxMul;
-            for (int rw = warp * rpw + rsub; rw < nrows; rw += (kThreads3 / 32) * rpw) {
+            for (int rw = wv * rpw + rsub; rw < nrows; rw += (kThreads3 / 32) * rpw) {
                 const int cz = (rw * cdiv) >> 16, cy = rw - cz * ncy;
                 const uint64_t p = px + static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul +
                                    static_cast<uint64_t>(static_cast<uint32_t>(cz)) * kIzMul;
@@ -198,7 +202,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 map_height4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
                 *reinterpret_cast<float4*>(g + cz * plane + cy * pitch + 4 * cg) = make_float4(h[0], h[1], h[2], h[3]);
             }
-            for (int rw = tid; rw < nrows; rw += kThreads3) {
+            for (int rw = tv; rw < nrows; rw += kThreads3) {
                 const int cz = (rw * cdiv) >> 16, cy = rw - cz * ncy;
                 g[cz * plane + cy * pitch + Wm] =
                     map_height(p0 + static_cast<uint64_t>(static_cast<uint32_t>(Wm)) * kIxMul +
