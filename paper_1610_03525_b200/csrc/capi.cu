@@ -107,6 +107,22 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
     const double w = c->has_gradient_weight ? c->gradient_weight : c->base_amplitude / 100.0;
     const bool zg = c->method == TG_METHOD_ZG_PAPER || c->method == TG_METHOD_ZG_SEPARABLE;
     int goff = 0, slot = 0;
+    // The aligned ppc-1 grid (the largest) goes first, at offset 0: the tile
+    // store stages each warp's rows over it (fbm2d.cu, FbmArgs::stage_pairs).
+    int o1 = -1;
+    int64_t size1 = 0;
+    if (plan_2d) {
+        for (int o = 0; o < c->octaves && o1 < 0; ++o) {
+            tg_octave_spec os;
+            octave_spec(c, o, &os);
+            if (os.fast && os.ppc == 1) {
+                o1 = o;
+                size1 = ((tg::kTileW + 1 + 3) & ~3) * static_cast<int64_t>(tg::kTileH + 1);
+                if (size1 > tg::kGridCap) o1 = -1;
+            }
+        }
+        if (o1 >= 0) goff = static_cast<int>(size1);
+    }
     for (int o = 0; o < c->octaves; ++o) {
         tg_octave_spec os;
         octave_spec(c, o, &os);
@@ -178,6 +194,16 @@ void plan_octaves(const tg_fbm_config* c, int64_t gmax, tg::OctDev* out, bool pl
         const int64_t pitch = (ncx + 3) & ~int64_t(3);
         const int64_t size = pitch * ncy;
         const bool needs_tab = mode == tg::kModeGrid;
+        if (o == o1 && ncx * ncy <= tg::kGridCap && size == size1 && !(needs_tab && slot >= tg::kTabSlots)) {
+            d.mode = mode;  // the reserved slot at offset 0
+            d.ncx = static_cast<int32_t>(ncx);
+            d.ncy = static_cast<int32_t>(ncy);
+            d.pitch = static_cast<int32_t>(pitch);
+            d.goff = 0;
+            d.cdiv = static_cast<int32_t>((65536 + ncx - 1) / ncx);
+            if (needs_tab) d.tslot = slot++;
+            continue;
+        }
         if (ncx * ncy > tg::kGridCap || goff + size > tg::kGridCap || (needs_tab && slot >= tg::kTabSlots)) {
             d.mode = tg::kModeDirect;
             continue;
@@ -357,6 +383,20 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
             }
         }
         a->ngroup[tg::kGProFine] = n;
+    }
+    // tile-store staging over the ppc-1 grid (plan_octaves puts it at offset 0)
+    a->stage_pairs = 0;
+    if (tg::fbm2d_tile_h() == 64) {
+        int below = 0, p1 = 0;
+        for (int o = 0; o < c->octaves; ++o) {
+            const tg::OctDev& d = a->oct[o];
+            const bool grid = d.mode == tg::kModePpc1 || d.mode == tg::kModeBlock2 || d.mode == tg::kModeBlock ||
+                              d.mode == tg::kModeGrid;
+            if (!grid) continue;
+            if (d.goff == 0 && d.lut_off == 0 && d.pitch >= tg::kTileW + 1 && d.pitch <= tg::kTileW + 4) p1 = 1;
+            else if (d.goff < tg::kTileW * 64) below = 1;
+        }
+        a->stage_pairs = p1 && !below;
     }
     a->lut = tg::row_lut(order_of(c));
     if (!a->lut) return fail(TG_EDEVICE, "row LUT allocation failed");

@@ -1256,7 +1256,16 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
     // Box start coordinates must be non-negative (negative ones fault), so a
     // warp whose rows start left of / above the window stores directly.
     const bool tma_warp = args.tma && tx0 >= args.ox && ty0 + r0 >= args.oy;
-    if (args.tma) __syncthreads();  // uniform per launch: every warp is done reading the corner grids
+    if (args.tma) {  // uniform per launch
+        if (args.stage_pairs) {
+            // warp w stages over ppc-1 corner rows 7.76w .. 7.76w + 7.75 (pitch
+            // 132): only warps w-1 and w read those, so w waits for w-1 alone
+            if (warp < kThreads / 32 - 1) asm volatile("bar.arrive %0, 64;" ::"r"(warp + 1) : "memory");
+            if (warp > 0) asm volatile("bar.sync %0, 64;" ::"r"(warp) : "memory");
+        } else {
+            __syncthreads();  // every warp is done reading the corner grids
+        }
+    }
     if (tma_warp) {
         float* stage = grid + r0 * kTW;
 #pragma unroll

@@ -142,6 +142,10 @@ struct FbmArgs {
     OctDev oct[kMaxOctaves];
     FineDev fine[kFineSlots];  // kGProFine octaves taken out of the list (see FineDev)
     BlkTDev blkt[kMaxCellSlots];
+    int32_t stage_pairs;       // the ppc-1 grid sits at offset 0 and no other grid below
+                               // kTileW * kTileH floats: the tile store's staging only
+                               // waits for the neighbouring warp (fbm2d.cu)
+    int32_t pad_;
 };
 
 struct Fbm3Args {
