@@ -381,6 +381,7 @@ def main() -> None:
         for i in range(10):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            torch.cuda._sleep(100000)  # ~50 us: e0 and the launch are queued before the GPU reaches e0
             e0.record(stream)
             launch(i)
             e1.record(stream)
