@@ -336,127 +336,152 @@ __global__ void boxcount_kernel(const uint32_t* __restrict__ bits, int64_t R, in
 
 // ---- variogram ----------------------------------------------------------------
 constexpr int kMaxLags = 32;
-constexpr int kFusedLags = 16;  // lags per fused pass (accumulators in registers)
+constexpr int kFusedLags = 16;  // lags per pass (accumulators in registers)
 
 struct LagSet {
     int n;
-    int h[kFusedLags];     // padded with 2^30 (never a pair)
-    int yoff[kFusedLags];  // h * ld, or -1: y-axis pairs done by variogram_y_kernel (h * ld >= 2^31)
+    int h[kFusedLags];  // padded with 2^30 (never a pair) for the x pass, 0 (self) for the y pass
 };
 
-constexpr int kSegC = 8192;    // columns per work item
+#ifndef TG_VG_SEGC
+#define TG_VG_SEGC 8192
+#endif
+constexpr int kSegC = TG_VG_SEGC;  // columns per x work item
 constexpr int kApron = 4096;   // x-lag partners beyond the segment kept in smem
 constexpr int kVgThreads = 256;
+constexpr int kYC = 4 * kVgThreads;  // columns per y work item (4 per thread)
 
-// All (lag, axis) pairs of up to 16 lags in ONE pass over the map.  A work
-// item is (row y, column segment [x0, x0 + C)); the segment plus an apron of
-// up to 4096 columns is widened to fp64 once into shared memory, so every
-// x-lag pair is two shared loads + DADD + DFMA with no conversion; y-lag
-// partners z(x, y+h) are coalesced global loads (CTAs sweep consecutive rows
-// together, so partner rows of lags up to a few hundred are L2 hits).  The
-// difference of two fp32 values is exact in fp64; sums are fp64.  Pairs whose
-// first point lies in rows [0, P) of a W x H window (P = H for a whole map;
-// P < H when the rows below a band were regenerated as lookahead).
-// sums[2*l + axis].
-// NL: lags in this pass (the set is padded to NL); kLongX: some x-lag exceeds
-// the apron (its partners are read from global memory).
+// x-axis pairs of up to 16 lags in ONE pass over the map.  A work item is
+// (row y, column segment [x0, x0 + C)); the segment plus an apron of up to
+// 4096 columns is widened to fp64 once into shared memory, so every x-lag
+// pair is two shared loads + DADD + DFMA with no conversion.  The difference
+// of two fp32 values is exact in fp64; sums are fp64.  Pairs whose first
+// point lies in rows [0, P) of a W x H window (P = H for a whole map; P < H
+// when the rows below a band were regenerated as lookahead).  sums[2*l].
+// kLongX: some lag exceeds the apron (its partners are read from global memory).
+#ifndef TG_VGX_MIN_BLOCKS
+#define TG_VGX_MIN_BLOCKS 2
+#endif
 template <int NL, bool kLongX>
-__global__ void __launch_bounds__(kVgThreads, 2)
-variogram_seg_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld, int64_t P,
-                     const __grid_constant__ LagSet L, int64_t nseg, int seg_cap,
-                     double* __restrict__ sums) {
+__global__ void __launch_bounds__(kVgThreads, TG_VGX_MIN_BLOCKS)
+variogram_x_kernel(const float* __restrict__ z, int64_t W, int64_t ld, int64_t P,
+                   const __grid_constant__ LagSet L, int64_t nseg, int seg_cap, double* __restrict__ sums) {
     extern __shared__ double seg[];
-    double ax[NL], ay[NL];
+    double ax[NL];
 #pragma unroll
-    for (int l = 0; l < NL; ++l) ax[l] = ay[l] = 0.0;
+    for (int l = 0; l < NL; ++l) ax[l] = 0.0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t items = P * nseg;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int64_t y = it / nseg;
         const int64_t x0 = (it - y * nseg) * kSegC;
-        const int wl = static_cast<int>(W - x0);                              // columns from x0
-        const int hl = static_cast<int>(H - y < (1 << 30) ? H - y : (1 << 30));  // rows from y
+        const int wl = static_cast<int>(W - x0);  // columns from x0
         const int cw = wl < kSegC ? wl : kSegC;
         const int sw = wl < seg_cap ? wl : seg_cap;  // segment + apron
         const float* row = z + y * ld + x0;
-        int yo[NL];  // per-item partner offsets; 0 (partner = self, d = 0) where no pair
-#pragma unroll
-        for (int l = 0; l < NL; ++l) yo[l] = (L.yoff[l] >= 0 && L.h[l] < hl) ? L.yoff[l] : 0;
         __syncthreads();  // previous item's readers are done with seg
         for (int i = threadIdx.x; i < sw; i += kVgThreads) seg[i] = static_cast<double>(__ldg(row + i));
         __syncthreads();
-        for (int xb = warp * 128; xb < cw; xb += (kVgThreads / 32) * 128) {
-#pragma unroll 1
-            for (int j = 0; j < 4; ++j) {
-                const int x = xb + 32 * j + lane;
-                if (x >= cw) break;
-                const float* rp = row + x;
-                float py[NL];
+        for (int x = threadIdx.x; x < cw; x += kVgThreads) {
+            const double v = seg[x];
 #pragma unroll
-                for (int l = 0; l < NL; ++l) py[l] = __ldg(rp + yo[l]);
-                const double v = seg[x];
-#pragma unroll
-                for (int l = 0; l < NL; ++l) {
-                    const int h = L.h[l];
-                    if (x + h < wl) {
-                        // without kLongX every h <= kApron, so x + h < sw: in smem
-                        const double p = (kLongX && x + h >= sw) ? static_cast<double>(__ldg(rp + h)) : seg[x + h];
-                        const double d = p - v;
-                        ax[l] = fma(d, d, ax[l]);
-                    }
-                    const double d = static_cast<double>(py[l]) - v;
-                    ay[l] = fma(d, d, ay[l]);
+            for (int l = 0; l < NL; ++l) {
+                const int h = L.h[l];
+                if (x + h < wl) {
+                    // without kLongX every h <= kApron, so x + h < sw: in smem
+                    const double p = (kLongX && x + h >= sw) ? static_cast<double>(__ldg(row + x + h)) : seg[x + h];
+                    const double d = p - v;
+                    ax[l] = fma(d, d, ax[l]);
                 }
             }
         }
     }
     __syncthreads();
-    double* part = seg;  // [8 warps][32]
+    double* part = seg;  // [8 warps][16]
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
-        double a = ax[l], b = ay[l];
-        for (int o = 16; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if (lane == 0) {
-            part[warp * 2 * kFusedLags + 2 * l] = a;
-            part[warp * 2 * kFusedLags + 2 * l + 1] = b;
-        }
+        double a = ax[l];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) part[warp * kFusedLags + l] = a;
     }
     __syncthreads();
-    if (threadIdx.x < 2 * L.n) {
+    if (threadIdx.x < L.n) {
         double t = 0.0;
-        for (int w = 0; w < kVgThreads / 32; ++w) t += part[w * 2 * kFusedLags + threadIdx.x];
-        atomicAdd(&sums[threadIdx.x], t);
+        for (int w = 0; w < kVgThreads / 32; ++w) t += part[w * kFusedLags + threadIdx.x];
+        atomicAdd(&sums[2 * threadIdx.x], t);
     }
 }
 
-// y-axis pairs of lags whose row offset h * ld does not fit 32 bits
-// (blockIdx.y = entry of `which`), one fp64 partial per block.
-__global__ void variogram_y_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld, int64_t P,
-                                   const __grid_constant__ LagSet L, double* __restrict__ sums) {
-    const int l = blockIdx.y;
-    if (L.yoff[l] >= 0) return;  // done by the fused kernel
-    const int64_t h = L.h[l];
-    const int64_t ny = min(P, H - h);
-    double acc = 0.0;
-    for (int64_t y = blockIdx.x; y < ny; y += gridDim.x) {
-        const float* a = z + y * ld;
-        const float* b = a + h * ld;
-        for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
-            const double d = static_cast<double>(b[x]) - static_cast<double>(a[x]);
-            acc = fma(d, d, acc);
+// y-axis pairs of up to 16 lags: a work item is (row y, 1024 columns), each
+// thread 4 consecutive columns as one 16-byte load per row; the partner rows
+// y + h of all lags are loaded back to back (64-bit row offsets, any ld), a
+// lag without a partner row reads its own row (d = 0, adds nothing), so the
+// loads of all lags are in flight together.  sums[2*l + 1].
+#ifndef TG_VGY_MIN_BLOCKS
+#define TG_VGY_MIN_BLOCKS 4
+#endif
+template <int NL, bool kVec>
+__global__ void __launch_bounds__(kVgThreads, TG_VGY_MIN_BLOCKS)
+variogram_y_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld, int64_t P,
+                   const __grid_constant__ LagSet L, double* __restrict__ sums) {
+    double ay[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) ay[l] = 0.0;
+    const int64_t nchunk = (W + kYC - 1) / kYC;
+    const int64_t items = P * nchunk;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t y = it / nchunk;
+        const int64_t x = (it - y * nchunk) * kYC + 4 * threadIdx.x;
+        if (x >= W) continue;
+        const int nv = W - x < 4 ? static_cast<int>(W - x) : 4;
+        const float* row = z + y * ld + x;
+        auto load = [&](const float* q, float (&o)[4]) {
+            if (kVec && nv == 4) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(q));
+                o[0] = t.x;
+                o[1] = t.y;
+                o[2] = t.z;
+                o[3] = t.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] = k < nv ? __ldg(q + k) : 0.f;
+            }
+        };
+        float a[4];
+        load(row, a);
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = static_cast<double>(a[k]);
+#pragma unroll
+        for (int g = 0; g < NL; g += 4) {  // 4 partner rows in flight per group
+            float b[4][4];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int64_t h = L.h[g + l];
+                load(y + h < H ? row + h * ld : row, b[l]);
+            }
+#pragma unroll
+            for (int l = 0; l < 4; ++l)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double d = static_cast<double>(b[l][k]) - v[k];
+                    ay[g + l] = fma(d, d, ay[g + l]);
+                }
         }
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    __shared__ double part[32];
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __shared__ double part[kVgThreads / 32][kFusedLags];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        double a = ay[l];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) part[warp][l] = a;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < L.n) {
         double t = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
-        atomicAdd(&sums[2 * l + 1], t);
+        for (int w = 0; w < kVgThreads / 32; ++w) t += part[w][threadIdx.x];
+        atomicAdd(&sums[2 * threadIdx.x + 1], t);
     }
 }
 
@@ -676,46 +701,48 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
     }
     const int64_t nseg = (width + kSegC - 1) / kSegC;
     const int seg_cap = static_cast<int>(std::min<int64_t>(width, kSegC + kApron));
-    const size_t smem = std::max<size_t>(static_cast<size_t>(seg_cap), 2 * kFusedLags * (kVgThreads / 32)) * sizeof(double);
+    const size_t smem = std::max<size_t>(static_cast<size_t>(seg_cap), kFusedLags * (kVgThreads / 32)) * sizeof(double);
+    using KX = void (*)(const float*, int64_t, int64_t, int64_t, LagSet, int64_t, int, double*);
+    using KY = void (*)(const float*, int64_t, int64_t, int64_t, int64_t, LagSet, double*);
+    static const KX xt[2][4] = {
+        {variogram_x_kernel<4, false>, variogram_x_kernel<8, false>, variogram_x_kernel<12, false>,
+         variogram_x_kernel<16, false>},
+        {variogram_x_kernel<4, true>, variogram_x_kernel<8, true>, variogram_x_kernel<12, true>,
+         variogram_x_kernel<16, true>}};
+    static const KY yt[2][4] = {
+        {variogram_y_kernel<4, false>, variogram_y_kernel<8, false>, variogram_y_kernel<12, false>,
+         variogram_y_kernel<16, false>},
+        {variogram_y_kernel<4, true>, variogram_y_kernel<8, true>, variogram_y_kernel<12, true>,
+         variogram_y_kernel<16, true>}};
     static bool attr_set = false;  // >48 KiB dynamic smem opt-in (idempotent)
     if (!attr_set) {
         const int mx = static_cast<int>((kSegC + kApron) * sizeof(double));
-        for (auto f : {variogram_seg_kernel<4, false>, variogram_seg_kernel<8, false>, variogram_seg_kernel<12, false>,
-                       variogram_seg_kernel<16, false>, variogram_seg_kernel<4, true>, variogram_seg_kernel<8, true>,
-                       variogram_seg_kernel<12, true>, variogram_seg_kernel<16, true>})
-            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        for (auto& r : xt)
+            for (auto f : r) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         attr_set = true;
     }
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, 2 * static_cast<int64_t>(sm)));
-    // passes of <= 12 lags, balanced (13 lags -> 7 + 6: the 16-lag variant
-    // runs out of registers)
-    const int passes = (n_lags + 11) / 12, per_pass = (n_lags + passes - 1) / passes;
-    for (int l0 = 0; l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += per_pass) {
-        LagSet L{};
-        L.n = std::min(per_pass, n_lags - l0);
-        bool long_x = false, long_y = false;
+    const int64_t xblocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, 2 * static_cast<int64_t>(sm)));
+    const int64_t nchunk = (width + kYC - 1) / kYC;
+    const int64_t yblocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nchunk, 8 * static_cast<int64_t>(sm)));
+    const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dev_map) & 15) == 0;
+    for (int l0 = 0; l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += kFusedLags) {
+        const int n = std::min(kFusedLags, n_lags - l0);
+        LagSet Lx{}, Ly{};
+        Lx.n = Ly.n = n;
+        bool long_x = false;
         for (int i = 0; i < kFusedLags; ++i) {
-            const int64_t h = i < L.n ? lags[l0 + i] : 0;
-            const bool pad = i >= L.n || h >= (int64_t(1) << 30);  // >= 2^30: no pair on either axis
-            L.h[i] = pad ? (1 << 30) : static_cast<int>(h);
-            const bool wide = !pad && h * ld >= (int64_t(1) << 31);
-            L.yoff[i] = pad ? 0 : wide ? -1 : static_cast<int>(h * ld);
+            const int64_t h = i < n ? lags[l0 + i] : 0;
+            const bool pad = i >= n || h >= (int64_t(1) << 30);  // >= 2^30: no pair on either axis
+            Lx.h[i] = pad ? (1 << 30) : static_cast<int>(h);
+            Ly.h[i] = pad ? 0 : static_cast<int>(h);  // 0: the row itself (d = 0)
             long_x = long_x || (!pad && h > kApron);
-            long_y = long_y || (wide && h < height);
         }
-        if (long_y) {
-            variogram_y_kernel<<<dim3(2 * sm, static_cast<unsigned>(L.n)), 256, 0, s>>>(
-                dev_map, width, height, ld, pair_rows, L, sums + 2 * l0);
-            if ((e = cudaGetLastError()) != cudaSuccess) break;
-        }
-        using K = void (*)(const float*, int64_t, int64_t, int64_t, int64_t, LagSet, int64_t, int, double*);
-        static const K table[2][4] = {
-            {variogram_seg_kernel<4, false>, variogram_seg_kernel<8, false>, variogram_seg_kernel<12, false>,
-             variogram_seg_kernel<16, false>},
-            {variogram_seg_kernel<4, true>, variogram_seg_kernel<8, true>, variogram_seg_kernel<12, true>,
-             variogram_seg_kernel<16, true>}};
-        table[long_x ? 1 : 0][(L.n - 1) / 4]<<<static_cast<unsigned>(blocks), kVgThreads, smem, s>>>(
-            dev_map, width, height, ld, pair_rows, L, nseg, seg_cap, sums + 2 * l0);
+        const int vi = (n - 1) / 4;
+        xt[long_x ? 1 : 0][vi]<<<static_cast<unsigned>(xblocks), kVgThreads, smem, s>>>(
+            dev_map, width, ld, pair_rows, Lx, nseg, seg_cap, sums + 2 * l0);
+        if ((e = cudaGetLastError()) != cudaSuccess) break;
+        yt[vec ? 1 : 0][vi]<<<static_cast<unsigned>(yblocks), kVgThreads, 0, s>>>(dev_map, width, height, ld,
+                                                                                  pair_rows, Ly, sums + 2 * l0);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_sum_sq, sums, 2 * n_lags * sizeof(double), cudaMemcpyDeviceToHost, s);
