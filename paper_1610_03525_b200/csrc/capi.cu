@@ -635,14 +635,17 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     const int64_t nb = (extent + band - 1) / band;
     const bool pinned = is_pinned(host_out);
     const bool direct32 = !f64 && pinned;  // fp32 into pinned: one DMA per band
-    // Pinned f64 destination: bands are widened on the device and DMA'd as f64
-    // straight into the caller's buffer (8 B/sample on the bus, no host work).
-    // TG_HOST_WIDEN_FRAC moves a fraction of them to the fp32 + host-widen
-    // route; measured on the B200 host (tools/time_e2e.py) that only trades
-    // PCIe for host memory bandwidth (2.27-2.5 ms vs 2.53 ms at 4096^2, with
-    // large run-to-run spread), so the default is 0.  Pageable destinations
-    // always take the host route (a pageable DMA is driver-staged anyway).
-    double frac = f64 ? (pinned ? env_double("TG_HOST_WIDEN_FRAC", 0.0) : 1.0) : 1.0;
+    // f64 destinations: bands cross PCIe as fp32 (4 B/sample) into the pinned
+    // staging ring and the host pool widens them into the caller's buffer
+    // while later bands are in flight.  With a pinned destination a fraction
+    // TG_HOST_WIDEN_FRAC of the bands may instead be widened on the device and
+    // DMA'd as f64 straight into it (8 B/sample, no host work): the default is
+    // all-host when the pool has >= 4 workers (config 2 on the B200 host:
+    // 1.5-1.6 ms vs 2.45 ms device-widened), all-device otherwise.  Pageable
+    // destinations always take the host route (a pageable DMA is
+    // driver-staged anyway).
+    const double frac_dflt = tg::host::threads() >= 4 ? 1.0 : 0.0;
+    double frac = f64 ? (pinned ? env_double("TG_HOST_WIDEN_FRAC", frac_dflt) : 1.0) : 1.0;
     frac = std::min(1.0, std::max(0.0, frac));
     auto host_widened = [&](int64_t i) {
         return std::floor(static_cast<double>(i + 1) * frac) > std::floor(static_cast<double>(i) * frac);

@@ -95,8 +95,14 @@ class Pool {
 
 Pool& pool() {
     static Pool* p = [] {
+        // Streaming widen/copy is host-memory-bound: on the B200 host (16
+        // hardware threads) 5-6 workers run fastest (f64 drop-in 1.5-1.6 ms),
+        // 8 already slower (2.0-2.4 ms) and 12 collapse (7-10 ms) as they
+        // contend with the CUDA driver and the caller for the same cores
+        // (tools/time_e2e.py).  Default: half the hardware threads minus two,
+        // at most 6.
         int n = static_cast<int>(std::thread::hardware_concurrency());
-        n = std::min(std::max(n, 1), 8);
+        n = std::min(std::max(n / 2 - 2, 1), 6);
         if (const char* e = std::getenv("TG_HOST_THREADS")) n = std::max(1, std::atoi(e));
         return new Pool(n);
     }();
