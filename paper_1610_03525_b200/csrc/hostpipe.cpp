@@ -100,9 +100,12 @@ Pool& pool() {
         // 8 already slower (2.0-2.4 ms) and 12 collapse (7-10 ms) as they
         // contend with the CUDA driver and the caller for the same cores
         // (tools/time_e2e.py).  Default: half the hardware threads minus two,
-        // at most 6.
+        // shared among the ranks of this node (LOCAL_WORLD_SIZE, set by
+        // torchrun), at most 6.
         int n = static_cast<int>(std::thread::hardware_concurrency());
-        n = std::min(std::max(n / 2 - 2, 1), 6);
+        int ranks = 1;
+        if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, std::atoi(e));
+        n = std::min(std::max((n / 2 - 2) / ranks, 1), 6);
         if (const char* e = std::getenv("TG_HOST_THREADS")) n = std::max(1, std::atoi(e));
         return new Pool(n);
     }();
