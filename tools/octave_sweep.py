@@ -31,6 +31,18 @@ def main():
     peak = pt.ffma_peak_tflops()
     hbm = bench.measured_hbm_gbs()
     bufs = [torch.empty((R, R), dtype=torch.float32, device="cuda") for _ in range(3)]
+    # write-only HBM bandwidth on the same buffers (torch fill_): the ceiling
+    # of a kernel that only writes its 64 MiB output
+    for i in range(10):
+        bufs[i % 3].fill_(1.0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(200):
+        bufs[i % 3].fill_(1.0)
+    e1.record()
+    torch.cuda.synchronize()
+    wpeak = 4 * R * R / (e0.elapsed_time(e1) / 200 * 1e-3) / 1e9
     rows = []
     for n in range(1, 17):
         cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=R, base_frequency=8,
@@ -50,11 +62,14 @@ def main():
         gbs = 4 * R * R / s / 1e9
         rows.append({"octaves": n, "us": s * 1e6, "sample_octaves_per_s": so, "tflops": tf,
                      "fp32_frac": tf / peak, "hbm_write_gbs": gbs, "hbm_frac": gbs / hbm,
+                     "write_frac_vs_fill": gbs / wpeak,
                      "hashes_per_sample": bench.hashes_per_launch(R, 8, n) / (R * R)})
         print(f"N={n:2d} {s*1e6:8.1f} us  {so/1e12:6.3f} T so/s  {tf:6.2f} TF ({tf/peak:5.1%})  "
               f"{gbs:7.1f} GB/s ({gbs/hbm:5.1%})", flush=True)
     res = {"workload": "4096^2 zg_paper S5, f0 = 8, ratio 2, persistence 0.5", "ffma_peak_tflops": peak,
-           "hbm_peak_gbs": hbm, "rows": rows}
+           "hbm_peak_gbs": hbm, "write_fill_gbs": wpeak,
+           "note": "hbm_frac against MEASURED_PEAKS.json hbm_gbs; write_frac_vs_fill against a torch fill_ of the "
+                   "same 64 MiB buffers measured in this run (write-only ceiling)", "rows": rows}
     if args.out:
         with open(args.out, "w") as f:
             json.dump(res, f, indent=1)
