@@ -1111,11 +1111,13 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             };
             Cell<KIND> cell;
             if (od.ppc >= kRPT) {
-                // the thread's rows lie in one cell: corners once per octave
+                // the thread's rows lie in one cell: corners once per octave;
+                // its rows are LUT entries (yo & mask) + r without wrap-around
                 load_cell(cell, yo >> sh);
+                const float4* Ly = L + (yo & mask);
 #pragma unroll
                 for (int r = 0; r < kRPT; ++r) {
-                    const float4 f = L[(yo + r) & mask];
+                    const float4 f = Ly[r];
                     accum(r, cell.row(f.x, f.y));
                 }
             } else {
