@@ -283,9 +283,9 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch
 // independent hash chains, keys advanced by +K3, one 16-byte store per
 // channel), rows strided over the warps starting at warp `rot`; the last
 // column and row go one corner per thread starting at thread 32 * rot.
-template <int SH, int CH, class GV>
+template <int SH, int CH, bool SCALE = false, class GV>
 __device__ __forceinline__ void fine_grid(float* g, int pitch, uint64_t p0, int warp, int lane, int tid, int rot,
-                                          GV& grid_value, const OctDev& od) {
+                                          GV& grid_value, const OctDev& od, float scale = 1.0f) {
     constexpr int Wm = kTileW >> SH, Hm = kTileH >> SH;
     constexpr int LSH = 5 - SH;                   // log2(lanes per corner row) = log2(Wm / 4)
     constexpr int RSTEP = 8 << SH;                // corner rows per pass over the 8 warps
@@ -305,7 +305,7 @@ __device__ __forceinline__ void fine_grid(float* g, int pitch, uint64_t p0, int 
                 float h[4];
                 map_height4(p, add64(p, kIxMul), add64(p, 2 * kIxMul), add64(p, 3 * kIxMul), h);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) d[u][0] = h[u];
+                for (int u = 0; u < 4; ++u) d[u][0] = SCALE ? scale * h[u] : h[u];
             } else {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) grid_value(add64(p, u * kIxMul), od, d[u]);
@@ -327,7 +327,7 @@ __device__ __forceinline__ void fine_grid(float* g, int pitch, uint64_t p0, int 
                        static_cast<uint64_t>(static_cast<uint32_t>(cy)) * kIyMul,
                    od, d);
 #pragma unroll
-        for (int c = 0; c < CH; ++c) g[c * kGridCap + cy * pitch + cx] = d[c];
+        for (int c = 0; c < CH; ++c) g[c * kGridCap + cy * pitch + cx] = SCALE ? scale * d[c] : d[c];
     }
 }
 
@@ -511,7 +511,13 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const uint64_t p0 = seed_key + fd.key0 + static_cast<uint64_t>(blockIdx.x) * fd.kx +
                             static_cast<uint64_t>(blockIdx.y) * fd.ky;
         float* g = grid + fd.goff;
-        fine_grid<SH, CH>(g, fd.pitch, p0, warp, lane, tid, fd.rot, grid_value, args.oct[fd.oct]);
+        if constexpr (kZg && SH == 1) {
+            // the ppc-2 grid is stored amplitude-scaled (its corner blends read it as is)
+            const float sc = args.oct[fd.oct].amp * kMapScale;
+            fine_grid<SH, CH, true>(g, fd.pitch, p0, warp, lane, tid, fd.rot, grid_value, args.oct[fd.oct], sc);
+        } else {
+            fine_grid<SH, CH>(g, fd.pitch, p0, warp, lane, tid, fd.rot, grid_value, args.oct[fd.oct]);
+        }
     };
     // (generic keeps its aligned grids in the list below: one runtime-shaped
     // copy of the 3-lane corner hash, two lanes with sincos — five
@@ -800,14 +806,20 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 R1[r + 4] = fmaf(sv[r], qB, R1[r + 4]);
             }
         }
+        // column constants of the two cell-row halves, the common term folded in
+        float CA[4], CB[4], C1B[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            CA[j] = C0[j] + hsum;
+            CB[j] = CA[j] + D0[j];
+            C1B[j] = C1[j] + D1[j];
+        }
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
-            const float rr = R0[r] + hsum;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                float v = C0[j] + rr;
-                if (r >= 4) v += D0[j];
-                if (r) v = fmaf(static_cast<float>(r), r >= 4 ? C1[j] + D1[j] : C1[j], v);
+                float v = (r >= 4 ? CB[j] : CA[j]) + R0[r];
+                if (r) v = fmaf(static_cast<float>(r), r >= 4 ? C1B[j] : C1[j], v);
                 if (j) v = fmaf(static_cast<float>(j), R1[r], v);
                 acc[r][j] = v;
             }
@@ -887,17 +899,17 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         for (int q = 0; q < TG_NG(kGBlk2, 32); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk2][q]];
             const int pitch = od.pitch;
-            const float sc = od.amp * kMapScale;
+            // the grid holds amplitude-scaled heights (fine slot 1)
             const float* g = grid + od.goff + (r0 >> 1) * pitch + (c0 >> 1);
             float t[3];
 #pragma unroll
-            for (int u = 0; u < 3; ++u) t[u] = sc * g[u];
+            for (int u = 0; u < 3; ++u) t[u] = g[u];
 #pragma unroll
             for (int k = 0; k < kRPT / 2; ++k) {
                 const float* gn = g + (k + 1) * pitch;
                 float b[3];
 #pragma unroll
-                for (int u = 0; u < 3; ++u) b[u] = sc * gn[u];
+                for (int u = 0; u < 3; ++u) b[u] = gn[u];
 #pragma unroll
                 for (int iy = 0; iy < 2; ++iy)
 #pragma unroll
