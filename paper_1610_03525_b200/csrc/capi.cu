@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -619,6 +620,11 @@ double env_double(const char* name, double dflt) {
 
 }  // namespace
 
+// Host widening cost (ns per element, running average over calls) and the
+// PCIe time of one fp32 element at ~52 GB/s (D2H on the B200 host).
+static std::atomic<double> g_widen_ns_per_elem{0.0};
+constexpr double kPcieNsPerF32 = 4.0 / 52.0;
+
 static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
                          void* host_out, uint64_t n_out, bool f64) {
     if (int st = validate_cfg(cfg)) return st;
@@ -647,7 +653,18 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     // 1.5-1.6 ms vs 2.45 ms device-widened), all-device otherwise.  Pageable
     // destinations always take the host route (a pageable DMA is
     // driver-staged anyway).
-    const double frac_dflt = tg::host::threads() >= 4 ? 1.0 : 0.0;
+    // Adaptive split for pinned f64 destinations: with P = PCIe time of an
+    // fp32 band and H = host widening time of a band (running average over
+    // calls), host-widening a fraction f of the bands costs
+    // max((2 - f) P, f H) per band, minimal at f = 2P / (P + H): all-host
+    // while the host keeps up (H <= P), shifting bands to device widening
+    // when the host's memory bandwidth is contended (measured bimodal on the
+    // shared B200 host: 1.38 vs 2.1-2.3 ms all-host at config 2).
+    double frac_dflt = 0.0;
+    if (tg::host::threads() >= 4) {
+        const double h = g_widen_ns_per_elem.load(std::memory_order_relaxed);
+        frac_dflt = h > 0.0 ? std::min(1.0, 2.0 * kPcieNsPerF32 / (kPcieNsPerF32 + h)) : 1.0;
+    }
     double frac = f64 ? (pinned ? env_double("TG_HOST_WIDEN_FRAC", frac_dflt) : 1.0) : 1.0;
     frac = std::min(1.0, std::max(0.0, frac));
     auto host_widened = [&](int64_t i) {
@@ -668,7 +685,16 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
         const int64_t y0 = j * band, h = std::min<int64_t>(band, extent - y0);
         const size_t n = static_cast<size_t>(h) * static_cast<size_t>(extent);
         const size_t off = static_cast<size_t>(y0) * static_cast<size_t>(extent);
-        if (f64) tg::host::widen(s->pin[slot], static_cast<double*>(host_out) + off, n, nt);
+        if (f64) {
+            const auto t0 = std::chrono::steady_clock::now();
+            tg::host::widen(s->pin[slot], static_cast<double*>(host_out) + off, n, nt);
+            const double ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+            if (n >= (size_t(1) << 18)) {  // running average of the host widening cost
+                const double prev = g_widen_ns_per_elem.load(std::memory_order_relaxed);
+                const double cur = ns / static_cast<double>(n);
+                g_widen_ns_per_elem.store(prev > 0.0 ? 0.75 * prev + 0.25 * cur : cur, std::memory_order_relaxed);
+            }
+        }
         else tg::host::copy(s->pin[slot], static_cast<float*>(host_out) + off, n, nt);
     };
     tg::FbmArgs a;
