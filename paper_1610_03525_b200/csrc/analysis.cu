@@ -340,7 +340,8 @@ constexpr int kFusedLags = 16;  // lags per pass (accumulators in registers)
 
 struct LagSet {
     int n;
-    int h[kFusedLags];  // padded with 2^30 (never a pair) for the x pass, 0 (self) for the y pass
+    int hmax;           // largest real lag of the set
+    int h[kFusedLags];  // padded with 0 (the sample itself, d = 0) on both axes
 };
 
 #ifndef TG_VG_SEGC
@@ -349,7 +350,7 @@ struct LagSet {
 constexpr int kSegC = TG_VG_SEGC;  // columns per x work item
 constexpr int kApron = 4096;   // x-lag partners beyond the segment kept in smem
 constexpr int kVgThreads = 256;
-constexpr int kYC = 4 * kVgThreads;  // columns per y work item (4 per thread)
+constexpr int kYC = 4 * kVgThreads;  // columns per y column strip (4 per thread)
 
 // x-axis pairs of up to 16 lags in ONE pass over the map.  A work item is
 // (row y, column segment [x0, x0 + C)); the segment plus an apron of up to
@@ -358,6 +359,8 @@ constexpr int kYC = 4 * kVgThreads;  // columns per y work item (4 per thread)
 // of two fp32 values is exact in fp64; sums are fp64.  Pairs whose first
 // point lies in rows [0, P) of a W x H window (P = H for a whole map; P < H
 // when the rows below a band were regenerated as lookahead).  sums[2*l].
+// An item whose every pair lies inside the row (all but the last segment of
+// a row) runs without per-pair bounds checks.
 // kLongX: some lag exceeds the apron (its partners are read from global memory).
 #ifndef TG_VGX_MIN_BLOCKS
 #define TG_VGX_MIN_BLOCKS 2
@@ -375,23 +378,36 @@ variogram_x_kernel(const float* __restrict__ z, int64_t W, int64_t ld, int64_t P
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int64_t y = it / nseg;
         const int64_t x0 = (it - y * nseg) * kSegC;
-        const int wl = static_cast<int>(W - x0);  // columns from x0
+        const int wl = static_cast<int>(W - x0 < (int64_t(1) << 30) ? W - x0 : (int64_t(1) << 30));  // columns from x0
         const int cw = wl < kSegC ? wl : kSegC;
         const int sw = wl < seg_cap ? wl : seg_cap;  // segment + apron
         const float* row = z + y * ld + x0;
         __syncthreads();  // previous item's readers are done with seg
         for (int i = threadIdx.x; i < sw; i += kVgThreads) seg[i] = static_cast<double>(__ldg(row + i));
         __syncthreads();
-        for (int x = threadIdx.x; x < cw; x += kVgThreads) {
-            const double v = seg[x];
+        if (!kLongX && cw + L.hmax <= wl) {
+            // interior item: every partner x + h < cw + hmax <= min(wl, seg_cap)
+            for (int x = threadIdx.x; x < cw; x += kVgThreads) {
+                const double v = seg[x];
 #pragma unroll
-            for (int l = 0; l < NL; ++l) {
-                const int h = L.h[l];
-                if (x + h < wl) {
-                    // without kLongX every h <= kApron, so x + h < sw: in smem
-                    const double p = (kLongX && x + h >= sw) ? static_cast<double>(__ldg(row + x + h)) : seg[x + h];
-                    const double d = p - v;
+                for (int l = 0; l < NL; ++l) {
+                    const double d = seg[x + L.h[l]] - v;
                     ax[l] = fma(d, d, ax[l]);
+                }
+            }
+        } else {
+            for (int x = threadIdx.x; x < cw; x += kVgThreads) {
+                const double v = seg[x];
+#pragma unroll
+                for (int l = 0; l < NL; ++l) {
+                    const int h = L.h[l];
+                    if (x + h < wl) {
+                        // without kLongX every h <= kApron, so x + h < sw: in smem
+                        const double p =
+                            (kLongX && x + h >= sw) ? static_cast<double>(__ldg(row + x + h)) : seg[x + h];
+                        const double d = p - v;
+                        ax[l] = fma(d, d, ax[l]);
+                    }
                 }
             }
         }
@@ -412,14 +428,87 @@ variogram_x_kernel(const float* __restrict__ z, int64_t W, int64_t ld, int64_t P
     }
 }
 
-// y-axis pairs of up to 16 lags: a work item is (row y, 1024 columns), each
-// thread 4 consecutive columns as one 16-byte load per row; the partner rows
-// y + h of all lags are loaded back to back (64-bit row offsets, any ld), a
-// lag without a partner row reads its own row (d = 0, adds nothing), so the
-// loads of all lags are in flight together.  sums[2*l + 1].
+// y-axis pairs of up to 16 lags.  A work item is (column strip of 1024) x
+// (kYRows rows); the CTA walks its strip down the rows, each thread 4
+// consecutive columns as one 16-byte load per row, so the partner rows of the
+// short lags are still in L1 from the previous rows, and items are handed out
+// grid-stride (one index division per item, no wave tail at any map shape).
+// The partner rows y + h of all lags are loaded back to back (64-bit row
+// offsets, any ld); a lag without a partner row reads its own row (d = 0,
+// adds nothing).  sums[2*l + 1].
 #ifndef TG_VGY_MIN_BLOCKS
-#define TG_VGY_MIN_BLOCKS 4
+#define TG_VGY_MIN_BLOCKS 3
 #endif
+#ifndef TG_VGY_NEAR
+#define TG_VGY_NEAR (1 << 30)
+#endif
+constexpr int kNearRows = TG_VGY_NEAR;
+#ifndef TG_VGY_ROWS
+#define TG_VGY_ROWS 32
+#endif
+constexpr int kYRows = TG_VGY_ROWS;  // rows per y work item (one column strip)
+template <int NL, bool kFull>
+__device__ __forceinline__ void variogram_y_rows(const float* __restrict__ row, int64_t y, int64_t y1, int64_t H,
+                                                 int64_t ld, int nv, const LagSet& L, double (&ay)[NL]) {
+    // Partner rows of lags beyond kNearRows bypass L1 (L1::no_allocate) so the
+    // near rows stay resident there until the walk reaches them.
+    auto load_far = [&](const float* q, float (&o)[4]) {
+        if (kFull) {
+            asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3])
+                         : "l"(q));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] = k < nv ? __ldg(q + k) : 0.f;
+        }
+    };
+    auto load = [&](const float* q, float (&o)[4]) {
+        if (kFull) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(q));
+            o[0] = t.x;
+            o[1] = t.y;
+            o[2] = t.z;
+            o[3] = t.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] = k < nv ? __ldg(q + k) : 0.f;
+        }
+    };
+    for (; y < y1; ++y, row += ld) {
+        float a[4];
+        load(row, a);
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = static_cast<double>(a[k]);
+#pragma unroll
+        for (int g = 0; g < NL; g += 4) {  // up to 4 partner rows in flight per group
+            constexpr int kG = 4;
+            float b[kG][4];
+#pragma unroll
+            for (int l = 0; l < kG; ++l) {
+                if (g + l < NL) {
+                    const int64_t h = L.h[g + l];
+                    const float* q = y + h < H ? row + h * ld : row;
+                    if (h > kNearRows)
+                        load_far(q, b[l]);
+                    else
+                        load(q, b[l]);
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < kG; ++l) {
+                if (g + l < NL) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const double d = static_cast<double>(b[l][k]) - v[k];
+                        ay[g + l] = fma(d, d, ay[g + l]);
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int NL, bool kVec>
 __global__ void __launch_bounds__(kVgThreads, TG_VGY_MIN_BLOCKS)
 variogram_y_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld, int64_t P,
@@ -428,46 +517,19 @@ variogram_y_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld
 #pragma unroll
     for (int l = 0; l < NL; ++l) ay[l] = 0.0;
     const int64_t nchunk = (W + kYC - 1) / kYC;
-    const int64_t items = P * nchunk;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t y = it / nchunk;
-        const int64_t x = (it - y * nchunk) * kYC + 4 * threadIdx.x;
+    const int64_t nrb = (P + kYRows - 1) / kYRows;
+    for (int64_t it = blockIdx.x; it < nchunk * nrb; it += gridDim.x) {
+        const int64_t rb = it / nchunk;
+        const int64_t y0 = rb * kYRows;
+        const int64_t y1 = y0 + kYRows < P ? y0 + kYRows : P;
+        const int64_t x = (it - rb * nchunk) * kYC + 4 * threadIdx.x;
         if (x >= W) continue;
         const int nv = W - x < 4 ? static_cast<int>(W - x) : 4;
-        const float* row = z + y * ld + x;
-        auto load = [&](const float* q, float (&o)[4]) {
-            if (kVec && nv == 4) {
-                const float4 t = __ldg(reinterpret_cast<const float4*>(q));
-                o[0] = t.x;
-                o[1] = t.y;
-                o[2] = t.z;
-                o[3] = t.w;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) o[k] = k < nv ? __ldg(q + k) : 0.f;
-            }
-        };
-        float a[4];
-        load(row, a);
-        double v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = static_cast<double>(a[k]);
-#pragma unroll
-        for (int g = 0; g < NL; g += 4) {  // 4 partner rows in flight per group
-            float b[4][4];
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int64_t h = L.h[g + l];
-                load(y + h < H ? row + h * ld : row, b[l]);
-            }
-#pragma unroll
-            for (int l = 0; l < 4; ++l)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const double d = static_cast<double>(b[l][k]) - v[k];
-                    ay[g + l] = fma(d, d, ay[g + l]);
-                }
-        }
+        const float* row = z + y0 * ld + x;
+        if (kVec && nv == 4)
+            variogram_y_rows<NL, true>(row, y0, y1, H, ld, nv, L, ay);
+        else
+            variogram_y_rows<NL, false>(row, y0, y1, H, ld, nv, L, ay);
     }
     __shared__ double part[kVgThreads / 32][kFusedLags];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -704,16 +766,10 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
     const size_t smem = std::max<size_t>(static_cast<size_t>(seg_cap), kFusedLags * (kVgThreads / 32)) * sizeof(double);
     using KX = void (*)(const float*, int64_t, int64_t, int64_t, LagSet, int64_t, int, double*);
     using KY = void (*)(const float*, int64_t, int64_t, int64_t, int64_t, LagSet, double*);
-    static const KX xt[2][4] = {
-        {variogram_x_kernel<4, false>, variogram_x_kernel<8, false>, variogram_x_kernel<12, false>,
-         variogram_x_kernel<16, false>},
-        {variogram_x_kernel<4, true>, variogram_x_kernel<8, true>, variogram_x_kernel<12, true>,
-         variogram_x_kernel<16, true>}};
-    static const KY yt[2][4] = {
-        {variogram_y_kernel<4, false>, variogram_y_kernel<8, false>, variogram_y_kernel<12, false>,
-         variogram_y_kernel<16, false>},
-        {variogram_y_kernel<4, true>, variogram_y_kernel<8, true>, variogram_y_kernel<12, true>,
-         variogram_y_kernel<16, true>}};
+#define TG_VG_NL(K, B) K<2, B>, K<4, B>, K<6, B>, K<8, B>, K<10, B>, K<12, B>, K<14, B>, K<16, B>
+    static const KX xt[2][8] = {{TG_VG_NL(variogram_x_kernel, false)}, {TG_VG_NL(variogram_x_kernel, true)}};
+    static const KY yt[2][8] = {{TG_VG_NL(variogram_y_kernel, false)}, {TG_VG_NL(variogram_y_kernel, true)}};
+#undef TG_VG_NL
     static bool attr_set = false;  // >48 KiB dynamic smem opt-in (idempotent)
     if (!attr_set) {
         const int mx = static_cast<int>((kSegC + kApron) * sizeof(double));
@@ -723,21 +779,24 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
     }
     const int64_t xblocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, 2 * static_cast<int64_t>(sm)));
     const int64_t nchunk = (width + kYC - 1) / kYC;
-    const int64_t yblocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nchunk, 8 * static_cast<int64_t>(sm)));
+    // y: work items of (column strip of kYC) x (kYRows rows), one wave of resident CTAs
+    const int64_t yitems = nchunk * ((pair_rows + kYRows - 1) / kYRows);
+    const int64_t yblocks = std::max<int64_t>(1, std::min<int64_t>(yitems, TG_VGY_MIN_BLOCKS * static_cast<int64_t>(sm)));
     const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dev_map) & 15) == 0;
     for (int l0 = 0; l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += kFusedLags) {
         const int n = std::min(kFusedLags, n_lags - l0);
         LagSet Lx{}, Ly{};
         Lx.n = Ly.n = n;
+        Lx.hmax = Ly.hmax = 0;
         bool long_x = false;
         for (int i = 0; i < kFusedLags; ++i) {
             const int64_t h = i < n ? lags[l0 + i] : 0;
             const bool pad = i >= n || h >= (int64_t(1) << 30);  // >= 2^30: no pair on either axis
-            Lx.h[i] = pad ? (1 << 30) : static_cast<int>(h);
-            Ly.h[i] = pad ? 0 : static_cast<int>(h);  // 0: the row itself (d = 0)
+            Lx.h[i] = Ly.h[i] = pad ? 0 : static_cast<int>(h);  // 0: the sample itself (d = 0)
+            if (!pad) Lx.hmax = Ly.hmax = std::max(Lx.hmax, static_cast<int>(h));
             long_x = long_x || (!pad && h > kApron);
         }
-        const int vi = (n - 1) / 4;
+        const int vi = (n - 1) / 2;
         xt[long_x ? 1 : 0][vi]<<<static_cast<unsigned>(xblocks), kVgThreads, smem, s>>>(
             dev_map, width, ld, pair_rows, Lx, nseg, seg_cap, sums + 2 * l0);
         if ((e = cudaGetLastError()) != cudaSuccess) break;
