@@ -365,6 +365,15 @@ constexpr int kYC = 4 * kVgThreads;  // columns per y column strip (4 per thread
 #ifndef TG_VGX_MIN_BLOCKS
 #define TG_VGX_MIN_BLOCKS 2
 #endif
+#ifndef TG_VGX_GRID
+#define TG_VGX_GRID 2  // x CTAs per SM
+#endif
+#ifndef TG_VGY_GRID
+#define TG_VGY_GRID 3  // y CTAs per SM
+#endif
+#ifndef TG_VG_CONCURRENT
+#define TG_VG_CONCURRENT 0
+#endif
 template <int NL, bool kLongX>
 __global__ void __launch_bounds__(kVgThreads, TG_VGX_MIN_BLOCKS)
 variogram_x_kernel(const float* __restrict__ z, int64_t W, int64_t ld, int64_t P,
@@ -777,11 +786,31 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
             for (auto f : r) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         attr_set = true;
     }
-    const int64_t xblocks = std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, 2 * static_cast<int64_t>(sm)));
+    const int64_t xblocks =
+        std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, TG_VGX_GRID * static_cast<int64_t>(sm)));
     const int64_t nchunk = (width + kYC - 1) / kYC;
     // y: work items of (column strip of kYC) x (kYRows rows), one wave of resident CTAs
     const int64_t yitems = nchunk * ((pair_rows + kYRows - 1) / kYRows);
-    const int64_t yblocks = std::max<int64_t>(1, std::min<int64_t>(yitems, TG_VGY_MIN_BLOCKS * static_cast<int64_t>(sm)));
+    const int64_t yblocks = std::max<int64_t>(1, std::min<int64_t>(yitems, TG_VGY_GRID * static_cast<int64_t>(sm)));
+    // TG_VG_CONCURRENT: the y pass runs on a forked stream beside the x pass
+    // (their sums are disjoint).  Off: measured no gain (8192^2: 0.610 vs
+    // 0.618 ms; 32768^2: 10.20 vs 10.13 ms) since the x pass's shared loads and
+    // the y pass's global loads share the L1 data pipe.
+    cudaStream_t sy = s;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (TG_VG_CONCURRENT) {
+        thread_local cudaStream_t side[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && (side[dev] || cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking) == cudaSuccess) &&
+            cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess) {
+            sy = side[dev];
+            e = cudaEventRecord(fork, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(sy, fork, 0);
+            if (e != cudaSuccess) return set_cuda_error(e, "variogram fork");
+        }
+    }
     const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dev_map) & 15) == 0;
     for (int l0 = 0; l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += kFusedLags) {
         const int n = std::min(kFusedLags, n_lags - l0);
@@ -800,10 +829,17 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
         xt[long_x ? 1 : 0][vi]<<<static_cast<unsigned>(xblocks), kVgThreads, smem, s>>>(
             dev_map, width, ld, pair_rows, Lx, nseg, seg_cap, sums + 2 * l0);
         if ((e = cudaGetLastError()) != cudaSuccess) break;
-        yt[vec ? 1 : 0][vi]<<<static_cast<unsigned>(yblocks), kVgThreads, 0, s>>>(dev_map, width, height, ld,
+        yt[vec ? 1 : 0][vi]<<<static_cast<unsigned>(yblocks), kVgThreads, 0, sy>>>(dev_map, width, height, ld,
                                                                                   pair_rows, Ly, sums + 2 * l0);
         e = cudaGetLastError();
     }
+    if (sy != s) {  // join (also on error: the scratch is freed in stream order on s)
+        const cudaError_t ej = cudaEventRecord(join, sy);
+        const cudaError_t ew = ej == cudaSuccess ? cudaStreamWaitEvent(s, join, 0) : ej;
+        if (e == cudaSuccess) e = ew;
+    }
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_sum_sq, sums, 2 * n_lags * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return set_cuda_error(e, "variogram");
