@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/polyterrain_b200.h"
+#include "devattr.h"
 
 namespace tg {
 int set_error(int code, const char* msg);
@@ -779,13 +780,16 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
     static const KX xt[2][8] = {{TG_VG_NL(variogram_x_kernel, false)}, {TG_VG_NL(variogram_x_kernel, true)}};
     static const KY yt[2][8] = {{TG_VG_NL(variogram_y_kernel, false)}, {TG_VG_NL(variogram_y_kernel, true)}};
 #undef TG_VG_NL
-    static bool attr_set = false;  // >48 KiB dynamic smem opt-in (idempotent)
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;  // >48 KiB dynamic smem opt-in, per device
+    e = attr_set.run([&] {
         const int mx = static_cast<int>((kSegC + kApron) * sizeof(double));
-        for (auto& r : xt)
-            for (auto f : r) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        attr_set = true;
-    }
+        cudaError_t r = cudaSuccess;
+        for (auto& row : xt)
+            for (auto f : row)
+                if (r == cudaSuccess) r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return r;
+    });
+    if (e != cudaSuccess) return set_cuda_error(e, "variogram smem opt-in");
     const int64_t xblocks =
         std::max<int64_t>(1, std::min<int64_t>(pair_rows * nseg, TG_VGX_GRID * static_cast<int64_t>(sm)));
     const int64_t nchunk = (width + kYC - 1) / kYC;

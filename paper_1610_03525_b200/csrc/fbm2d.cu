@@ -30,6 +30,7 @@
 #include <mutex>
 #include <type_traits>
 
+#include "devattr.h"
 #include "fbm_params.h"
 #include "lattice.cuh"
 
@@ -1399,13 +1400,11 @@ template <int KIND, int ORDER, bool LEAN>
 static cudaError_t launch_v(const FbmArgs& a0, float* out, cudaStream_t st) {
     constexpr size_t smem = smem_bytes<KIND, LEAN>();
     auto kern = fbm2d_kernel<KIND, ORDER, LEAN>;
-    static bool configured = false;  // benign race: idempotent attribute set
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce configured;
+    cudaError_t e = configured.run([&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    });
+    if (e != cudaSuccess) return e;
     FbmArgs a = a0;
     CUtensorMap m;
     a.tma = TG_TMA_STORE && encode_out_map(a, out, &m) ? 1 : 0;

@@ -20,6 +20,7 @@
 
 #include <cmath>
 
+#include "devattr.h"
 #include "fbm_params.h"
 #include "lattice.cuh"
 
@@ -484,13 +485,12 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
 
 template <int ORDER, bool LEAN>
 cudaError_t launch3v(const Fbm3Args& a, float* out, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fbm3d_kernel<ORDER, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem3<LEAN>()));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce configured;
+    cudaError_t e = configured.run([] {
+        return cudaFuncSetAttribute(fbm3d_kernel<ORDER, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem3<LEAN>()));
+    });
+    if (e != cudaSuccess) return e;
     dim3 grid(static_cast<unsigned>((a.ox + a.nx - a.tile_x0 + kTX - 1) / kTX),
               static_cast<unsigned>((a.oy + a.ny - a.tile_y0 + kTY - 1) / kTY),
               static_cast<unsigned>((a.oz + a.nz - a.tile_z0 + kTZ - 1) / kTZ));

@@ -78,7 +78,11 @@ const float4* row_lut(int order) {
     }
     float4* d = nullptr;
     if (cudaMalloc(&d, sizeof(float4) * h.size()) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, h.data(), sizeof(float4) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    // A pageable cudaMemcpy may return before the DMA lands; the first
+    // generation launch can go onto a non-blocking stream that does not wait
+    // on the legacy stream, so complete the copy before publishing the LUT.
+    if (cudaMemcpy(d, h.data(), sizeof(float4) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
         cudaFree(d);
         return nullptr;
     }

@@ -17,6 +17,7 @@
 // per lookup.  Both give the same index, so the choice never changes a pixel.
 #include <cuda_runtime.h>
 
+#include "devattr.h"
 #include "fbm_params.h"
 #include "lattice.cuh"
 
@@ -220,11 +221,11 @@ cudaError_t simplex2d_launch(const FbmArgs& a, float* out, cudaStream_t st) {
             bytes += static_cast<int>((n + 15) / 16 * 16);
         }
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(simplex2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableMaxBytes);
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    cudaError_t e = attr.run([] {
+        return cudaFuncSetAttribute(simplex2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableMaxBytes);
+    });
+    if (e != cudaSuccess) return e;
     const int64_t tiles_x = (p.ox + p.width - p.tile_x0 + kTW - 1) / kTW;
     const int64_t tiles_y = (p.oy + p.height - p.tile_y0 + kTH - 1) / kTH;
     dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y), static_cast<unsigned>(p.n_maps));

@@ -172,14 +172,22 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream)
 
 
-def generate_into_device(cfg: FbmConfig, origin, extent: int, out, stream=None) -> None:
-    """Device form of generate_into (fbm.hpp:541-628): `out` is a CUDA fp32
-    tensor of extent^2 elements, written stream-ordered (no host sync)."""
+def _check_device_out(out, need: int) -> None:
+    """`out` must be a contiguous CUDA float32 tensor of at least `need`
+    elements (else ValidationError, never an out-of-bounds device write)."""
     import torch
 
     if not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float32
             and out.is_contiguous()):
         raise ValidationError("generate: output must be a contiguous CUDA float32 tensor")
+    if out.numel() < need:
+        raise ValidationError("generate: output buffer size mismatch")
+
+
+def generate_into_device(cfg: FbmConfig, origin, extent: int, out, stream=None) -> None:
+    """Device form of generate_into (fbm.hpp:541-628): `out` is a CUDA fp32
+    tensor of extent^2 elements, written stream-ordered (no host sync)."""
+    _check_device_out(out, int(extent) * int(extent))
     _check(_abi.load().tg_fbm_generate_f32(C.byref(cfg.to_c()), int(origin[0]), int(origin[1]),
                                             int(extent), out.data_ptr(), out.numel(),
                                             _stream_ptr(stream)))
@@ -189,6 +197,9 @@ def generate_rect_device(cfg: FbmConfig, origin, width: int, height: int, out, l
                          stream=None) -> None:
     """Rectangular window with row pitch `ld` (chunks and row bands)."""
     ld = width if ld is None else ld
+    if width < 1 or height < 1 or ld < width:
+        raise ValidationError("generate: bad window shape or row pitch")
+    _check_device_out(out, (int(height) - 1) * int(ld) + int(width))
     _check(_abi.load().tg_fbm_generate_rect_f32(C.byref(cfg.to_c()), int(origin[0]), int(origin[1]),
                                                  int(width), int(height), out.data_ptr(), int(ld),
                                                  _stream_ptr(stream)))
@@ -197,6 +208,9 @@ def generate_rect_device(cfg: FbmConfig, origin, width: int, height: int, out, l
 def generate_batch_device(cfg: FbmConfig, seeds: Sequence[int], origin, width: int, height: int, out,
                           stream=None) -> None:
     """Maps differing only in seed, one launch per 64 seeds."""
+    if width < 1 or height < 1:
+        raise ValidationError("generate: bad window shape")
+    _check_device_out(out, len(seeds) * int(width) * int(height))
     arr = (C.c_uint64 * len(seeds))(*[int(s) & 0xFFFFFFFFFFFFFFFF for s in seeds])
     _check(_abi.load().tg_fbm_generate_batch_f32(C.byref(cfg.to_c()), arr, len(seeds), int(origin[0]),
                                                   int(origin[1]), int(width), int(height),

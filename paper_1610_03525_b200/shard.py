@@ -46,6 +46,16 @@ class Band:
     height: int      # whole terrain height (rows)
     halo_top: int    # regenerated rows above (0 or 1)
     below: int       # regenerated rows below: max(halo, lookahead), clipped to the terrain
+    y_origin: int = 0  # global row of the terrain's first row (y0 - y_origin is band-local)
+    max_lag: int = 0   # lookahead the band was planned for (vertical variogram lags)
+
+    @property
+    def local_y0(self) -> int:
+        return self.y0 - self.y_origin
+
+    @property
+    def is_last(self) -> bool:
+        return self.local_y0 + self.rows >= self.height
 
     @property
     def gen_y0(self) -> int:
@@ -73,7 +83,7 @@ def plan_band(width: int, height: int, world: int, rank: int, align: int = 64, m
     y0, y1 = u0 * align, u1 * align
     halo_top = 1 if y0 > 0 else 0
     below = min(max(1, max_lag), height - y1)
-    return Band(rank, world, x0, width, y_origin + y0, y1 - y0, height, halo_top, below)
+    return Band(rank, world, x0, width, y_origin + y0, y1 - y0, height, halo_top, below, y_origin, max_lag)
 
 
 class Comm:
@@ -141,8 +151,11 @@ def terrain_stats(band: Band, backend, comm: Comm, sizes: Sequence[int], lags: S
     """Generate this rank's band (+ regenerated halo/lookahead rows) and
     reduce the fractal statistics of the whole terrain across ranks."""
     for s in sizes:
-        if band.y0 % s != 0 or (band.rows % s != 0 and band.y0 + band.rows != band.height):
+        if band.local_y0 % s != 0 or (band.rows % s != 0 and not band.is_last):
             raise ValidationError("terrain_stats: band starts/ends must be multiples of every box size")
+    if lags and max(lags) > band.below and not band.is_last:
+        raise ValidationError("terrain_stats: a variogram lag exceeds the band's regenerated lookahead "
+                              "(plan_band max_lag)")
     backend.generate(band)
     total = band.width * band.height
     if sea_level is None:
@@ -208,7 +221,7 @@ class DeviceBackend:
         arr = (C.c_int32 * len(sizes))(*sizes)
         cnt = (C.c_int64 * len(sizes))()
         coast, land = C.c_int64(), C.c_int64()
-        has_bot = 1 if b.y0 + b.rows < b.height else 0
+        has_bot = 0 if b.is_last else 1
         _check(_abi.load().tg_coastline_boxcount_band(self._owned_ptr(), b.width, b.rows, b.width, b.halo_top,
                                                       has_bot, float(sea), arr, len(sizes), cnt,
                                                       C.byref(coast), C.byref(land), self._sp()))
