@@ -13,6 +13,7 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -428,6 +429,72 @@ int or_generate(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, i
     return TG_OK;
 }
 
+/* or_generate split into row bands over `nthreads` host threads (test
+ * infrastructure: full-map parity at the BASELINE sizes).  Every pixel still
+ * accumulates its octaves 0..N-1 in order, so the result is bit-identical to
+ * or_generate; only the window origin is validated (the bands themselves need
+ * not be octave-0 aligned). */
+typedef struct {
+    const tg_fbm_config* c;
+    int64_t ox, oy, width, y0, y1;
+    int order;
+    double* out;
+} or_band;
+
+static void* or_band_main(void* p) {
+    const or_band* b = (const or_band*)p;
+    const tg_fbm_config* c = b->c;
+    for (int64_t ly = b->y0; ly < b->y1; ++ly) {
+        double* row = b->out + (size_t)ly * (size_t)b->width;
+        for (int64_t lx = 0; lx < b->width; ++lx) row[lx] = 0.0;
+    }
+    for (int oct = 0; oct < c->octaves; ++oct) {
+        tg_octave_spec os;
+        or_octave_spec(c, oct, &os);
+        for (int64_t ly = b->y0; ly < b->y1; ++ly) {
+            double* row = b->out + (size_t)ly * (size_t)b->width;
+            for (int64_t lx = 0; lx < b->width; ++lx)
+                row[lx] += os.fast && c->method != TG_METHOD_OPENSIMPLEX
+                               ? fast_sample(c, oct, &os, b->ox + lx, b->oy + ly, b->order)
+                               : general_sample(c, oct, &os, b->ox + lx, b->oy + ly, b->order);
+        }
+    }
+    return NULL;
+}
+
+int or_generate_mt(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, int64_t height,
+                   double* out, int32_t nthreads) {
+    if (or_validate(c) != TG_OK) return TG_EVALIDATION;
+    if (width < 1 || height < 1 || width > TG_MAX_EXTENT || height > TG_MAX_EXTENT)
+        return TG_EVALIDATION;
+    const int64_t origin[2] = {ox, oy};
+    for (int q = 0; q < 2; ++q) {
+        const int64_t o = origin[q];
+        if (o < -(1LL << 40) || o > (1LL << 40)) return TG_EVALIDATION;
+        const int64_t prod = o * c->base_frequency;
+        if (((prod % c->resolution) + c->resolution) % c->resolution != 0) return TG_EVALIDATION;
+    }
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    if (nthreads > height) nthreads = (int32_t)height;
+    or_band bands[256];
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) {
+        bands[t].c = c;
+        bands[t].ox = ox;
+        bands[t].oy = oy;
+        bands[t].width = width;
+        bands[t].y0 = height * t / nthreads;
+        bands[t].y1 = height * (t + 1) / nthreads;
+        bands[t].order = order_of(c);
+        bands[t].out = out;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, or_band_main, &bands[t]);
+    or_band_main(&bands[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+    return TG_OK;
+}
+
 /* The same per-pixel values as or_generate at arbitrary global pixels
  * (a window's value is a pure function of (cfg, global pixel), fbm.hpp:7-8);
  * used to spot-check maps too large for a full oracle pass. */
@@ -461,6 +528,38 @@ static void axis_coord(const tg_octave_spec* os, int64_t R, int64_t g, int64_t* 
     }
 }
 
+/* The separable zero-gradient 3D cell over corners h[q], q = x + 2y + 4z:
+ * lerp_z(lerp_y(lerp_x(h, Sx), Sy), Sz).  On the faces z = 0 / z = 1 it is
+ * the 2D zg_eval(..., ZgVariant::separable, order) of that face's corners
+ * (kernels2d.hpp:70-76), which tests/test_oracle_golden.py pins against the
+ * compiled reference. */
+double or_cell3(const double h[8], double x, double y, double z, int order) {
+    const double sx = or_smoothstep(order, x), sy = or_smoothstep(order, y),
+                 sz = or_smoothstep(order, z);
+    const double e00 = h[0] + sx * (h[1] - h[0]);
+    const double e10 = h[2] + sx * (h[3] - h[2]);
+    const double e01 = h[4] + sx * (h[5] - h[4]);
+    const double e11 = h[6] + sx * (h[7] - h[6]);
+    const double f0 = e00 + sy * (e10 - e00);
+    const double f1 = e01 + sy * (e11 - e01);
+    return f0 + sz * (f1 - f0);
+}
+
+static double voxel3(const tg_fbm_config* c, int oct, const tg_octave_spec* os, int64_t gx,
+                     int64_t gy, int64_t gz, int order) {
+    int64_t ix, iy, iz;
+    double x, y, z;
+    axis_coord(os, c->resolution, gx, &ix, &x);
+    axis_coord(os, c->resolution, gy, &iy, &y);
+    axis_coord(os, c->resolution, gz, &iz, &z);
+    double h[8];
+    for (int q = 0; q < 8; ++q)
+        h[q] = c->zero_lattice ? 0.0
+                               : os->amp * or_corner_height3(c->seed, (uint32_t)oct, ix + (q & 1),
+                                                             iy + ((q >> 1) & 1), iz + ((q >> 2) & 1));
+    return or_cell3(h, x, y, z, order);
+}
+
 int or_generate3d(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t oz, int64_t nx,
                   int64_t ny, int64_t nz, double* out) {
     if (or_validate(c) != TG_OK) return TG_EVALIDATION;
@@ -474,30 +573,24 @@ int or_generate3d(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t oz, in
         or_octave_spec(c, oct, &os);
         for (int64_t lz = 0; lz < nz; ++lz)
             for (int64_t ly = 0; ly < ny; ++ly)
-                for (int64_t lx = 0; lx < nx; ++lx) {
-                    int64_t ix, iy, iz;
-                    double x, y, z;
-                    axis_coord(&os, c->resolution, ox + lx, &ix, &x);
-                    axis_coord(&os, c->resolution, oy + ly, &iy, &y);
-                    axis_coord(&os, c->resolution, oz + lz, &iz, &z);
-                    double h[8];
-                    for (int q = 0; q < 8; ++q)
-                        h[q] = c->zero_lattice
-                                   ? 0.0
-                                   : os.amp * or_corner_height3(c->seed, (uint32_t)oct,
-                                                                ix + (q & 1), iy + ((q >> 1) & 1),
-                                                                iz + ((q >> 2) & 1));
-                    const double sx = or_smoothstep(order, x), sy = or_smoothstep(order, y),
-                                 sz = or_smoothstep(order, z);
-                    const double e00 = h[0] + sx * (h[1] - h[0]);
-                    const double e10 = h[2] + sx * (h[3] - h[2]);
-                    const double e01 = h[4] + sx * (h[5] - h[4]);
-                    const double e11 = h[6] + sx * (h[7] - h[6]);
-                    const double f0 = e00 + sy * (e10 - e00);
-                    const double f1 = e01 + sy * (e11 - e01);
+                for (int64_t lx = 0; lx < nx; ++lx)
                     out[((size_t)lz * (size_t)ny + (size_t)ly) * (size_t)nx + (size_t)lx] +=
-                        f0 + sz * (f1 - f0);
-                }
+                        voxel3(c, oct, &os, ox + lx, oy + ly, oz + lz, order);
+    }
+    return TG_OK;
+}
+
+/* or_generate3d's values at arbitrary global voxels. */
+int or_sample3d(const tg_fbm_config* c, const int64_t* gx, const int64_t* gy, const int64_t* gz,
+                int64_t n, double* out) {
+    if (or_validate(c) != TG_OK) return TG_EVALIDATION;
+    if (c->method != TG_METHOD_ZG_SEPARABLE) return TG_EVALIDATION;
+    const int order = order_of(c);
+    for (int64_t i = 0; i < n; ++i) out[i] = 0.0;
+    for (int oct = 0; oct < c->octaves; ++oct) {
+        tg_octave_spec os;
+        or_octave_spec(c, oct, &os);
+        for (int64_t i = 0; i < n; ++i) out[i] += voxel3(c, oct, &os, gx[i], gy[i], gz[i], order);
     }
     return TG_OK;
 }

@@ -73,6 +73,9 @@ class Oracle:
             "or_generate": (C.c_int, [PCFG, I64, I64, I64, I64, P]),
             "or_sample": (C.c_int, [PCFG, P, P, I64, P]),
             "or_generate3d": (C.c_int, [PCFG, I64, I64, I64, I64, I64, I64, P]),
+            "or_generate_mt": (C.c_int, [PCFG, I64, I64, I64, I64, P, I32]),
+            "or_sample3d": (C.c_int, [PCFG, P, P, P, I64, P]),
+            "or_cell3": (F64, [P, F64, F64, F64, C.c_int]),
             "or_normalize": (C.c_int, [P, I64, C.POINTER(F64), C.POINTER(F64), C.POINTER(C.c_int)]),
             "or_upper_median": (F64, [P, I64]),
             "or_coastline_mask": (C.c_int, [P, I64, F64, P, C.POINTER(I64)]),
@@ -129,6 +132,31 @@ class Oracle:
         if st != 0:
             raise ValueError(f"oracle generate: status {st}")
         return out
+
+    def generate_mt(self, cfg: TgFbmConfig, ox: int, oy: int, width: int, height: int | None = None,
+                    threads: int | None = None):
+        """or_generate over row bands on `threads` host threads (bit-identical)."""
+        height = width if height is None else height
+        threads = threads or os.cpu_count() or 1
+        out = np.empty((height, width), dtype=np.float64)
+        st = self.lib.or_generate_mt(C.byref(cfg), ox, oy, width, height, _ptr(out), threads)
+        if st != 0:
+            raise ValueError(f"oracle generate_mt: status {st}")
+        return out
+
+    def sample3d(self, cfg: TgFbmConfig, gx, gy, gz) -> np.ndarray:
+        x = np.ascontiguousarray(gx, dtype=np.int64)
+        y = np.ascontiguousarray(gy, dtype=np.int64)
+        z = np.ascontiguousarray(gz, dtype=np.int64)
+        out = np.zeros(len(x))
+        st = self.lib.or_sample3d(C.byref(cfg), _ptr(x), _ptr(y), _ptr(z), len(x), _ptr(out))
+        if st != 0:
+            raise ValueError(f"oracle sample3d: status {st}")
+        return out
+
+    def cell3(self, h, x: float, y: float, z: float, order: int) -> float:
+        hh = np.ascontiguousarray(h, dtype=np.float64)
+        return self.lib.or_cell3(_ptr(hh), x, y, z, order)
 
     def sample(self, cfg: TgFbmConfig, gx, gy) -> np.ndarray:
         x = np.ascontiguousarray(gx, dtype=np.int64)

@@ -480,6 +480,9 @@ def norm_map_device(dev_map, width: int, height: int, out, hessian: bool = False
 def generate3d_device(cfg: FbmConfig, origin, shape, out, stream=None) -> None:
     """3D fBm volume (new): out is a CUDA fp32 tensor [nz, ny, nx]."""
     nz, ny, nx = shape
+    if nx < 1 or ny < 1 or nz < 1:
+        raise ValidationError("generate3d: bad volume shape")
+    _check_device_out(out, int(nx) * int(ny) * int(nz))
     _check(_abi.load().tg_fbm3d_generate_f32(C.byref(cfg.to_c()), int(origin[0]), int(origin[1]), int(origin[2]),
                                              nx, ny, nz, out.data_ptr(), _stream_ptr(stream)))
 

@@ -120,32 +120,7 @@ def test_config1_full_map(oracle):
     check_close(m, oracle.generate(c, 0, 0, 1024), c, "cfg1")
 
 
-def test_config2_s5_4096(oracle):
-    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=4096, base_frequency=8, octaves=12)
-    m = gen(c, 0, 0, 4096)
-    check_close(m[:256, :256].cpu().numpy(), oracle.generate(c, 0, 0, 256), c, "cfg2 window")
-    # bottom-right corner block (windows must be octave-0 aligned, so sample it)
-    ys, xs = np.meshgrid(np.arange(4096 - 96, 4096), np.arange(4096 - 96, 4096), indexing="ij")
-    ref = oracle.sample(c, xs.ravel(), ys.ravel()).reshape(96, 96)
-    check_close(m[-96:, -96:].cpu().numpy(), ref, c, "cfg2 corner")
-    _sample_check(oracle, c, m, 0, 0)
-
-
-@pytest.mark.parametrize("method", [0, 1, 2, 3, 4])
-def test_config3_grid_all_methods(oracle, method):
-    c = make_cfg(method=method, seed=1, resolution=4096, base_frequency=8, octaves=12)
-    m = gen(c, 0, 0, 4096)
-    check_close(m[:128, :128].cpu().numpy(), oracle.generate(c, 0, 0, 128), c, f"cfg3 m{method}")
-    _sample_check(oracle, c, m, 0, 0, n=1024)
-
-
-def test_config5_chunk_32768(oracle):
-    # 32768^2 terrain, f0 = 32 (1024-px base cells = chunks), 16 octaves, S5.
-    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=32768, base_frequency=32, octaves=16)
-    ox, oy = 17 * 1024, 29 * 1024
-    m = gen(c, ox, oy, 1024)
-    check_close(m[:64, :64].cpu().numpy(), oracle.generate(c, ox, oy, 64), c, "cfg5 chunk")
-    _sample_check(oracle, c, m, ox, oy, n=2048)
+# config 2, 3 and 5 at their full shapes: tests/test_gpu_fullshape.py
 
 
 def test_config5_proxy_equals_golden(golden):
