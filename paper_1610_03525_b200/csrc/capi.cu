@@ -311,7 +311,7 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     a->octaves = c->octaves;
     a->zero = c->zero_lattice ? 1 : 0;
     a->n_maps = 1;
-    a->seed_key[0] = c->seed * tg::kSeedMul;
+    a->seed_key[0] = c->seed * tg::kSeedMul + tg::kMapKeyBias;
     int64_t gmax = 0;
     const int64_t cand[4] = {ox - 256, ox + width + 256, oy - 256, oy + height + 256};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);
@@ -507,7 +507,7 @@ int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, i
     for (int32_t b0 = 0; b0 < n_seeds; b0 += tg::kMaxBatch) {
         const int nb = std::min<int32_t>(tg::kMaxBatch, n_seeds - b0);
         a.n_maps = nb;
-        for (int i = 0; i < nb; ++i) a.seed_key[i] = seeds[b0 + i] * tg::kSeedMul;
+        for (int i = 0; i < nb; ++i) a.seed_key[i] = seeds[b0 + i] * tg::kSeedMul + tg::kMapKeyBias;
         TG_CUDA(tg::fbm2d_launch(kind_of(cfg), order_of(cfg), a,
                                  dev_out + static_cast<int64_t>(b0) * width * height,
                                  static_cast<cudaStream_t>(stream)));
@@ -774,7 +774,7 @@ int tg_fbm3d_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int6
     a.R = static_cast<double>(cfg->resolution);
     a.octaves = cfg->octaves;
     a.zero = cfg->zero_lattice ? 1 : 0;
-    a.seed_key = cfg->seed * tg::kSeedMul;
+    a.seed_key = cfg->seed * tg::kSeedMul + tg::kMapKeyBias;
     int64_t gmax = 0;
     const int64_t cand[6] = {ox - 64, ox + nx + 64, oy - 64, oy + ny + 64, oz - 64, oz + nz + 64};
     for (int64_t v : cand) gmax = std::max<int64_t>(gmax, v < 0 ? -v : v);

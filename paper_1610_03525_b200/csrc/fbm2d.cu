@@ -63,14 +63,14 @@ __device__ __forceinline__ void corner_data_packed(uint64_t p, float amp, float 
         d[0] = amp63 * map_height(p);
     } else if constexpr (KIND == kPerlin) {
         float c, s;
-        fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
+        fast_sincos_turns(unit_from_hash(mix64(p ^ kMapLane(kAngleLane))), &s, &c);
         d[0] = amp * c;
         d[1] = amp * s;
     } else {
         d[0] = amp63 * map_height(p);
         float c, s;
-        fast_sincos_turns(unit_from_hash(mix64(p ^ kAngleLane)), &s, &c);
-        const float m = unit_from_hash(mix64(p ^ kMagnitudeLane)) * w;
+        fast_sincos_turns(unit_from_hash(mix64(p ^ kMapLane(kAngleLane))), &s, &c);
+        const float m = unit_from_hash(mix64(p ^ kMapLane(kMagnitudeLane))) * w;
         d[1] = m * c;
         d[2] = m * s;
     }

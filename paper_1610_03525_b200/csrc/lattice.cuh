@@ -10,6 +10,20 @@
 
 #include <cstdint>
 
+#ifndef TG_MAP_HEIGHT_HI
+#define TG_MAP_HEIGHT_HI 1
+#endif
+// TG_MAP_SIGNED=1 (default): signed top word (sign flip in the last IMAD.HI
+// addend, I2FP.S32), height = f * 2^-31 with no per-octave offset, so the
+// fp32 partial sums stay at the magnitude of the map itself and the absolute
+// error scales with the window's own amplitude (north-star 1e-5 * A in every
+// 64 x 64 window, tests/test_gpu_fullshape.py).  0: unsigned word + the
+// -sum(amp) offset (FbmArgs::hoff) — the partial sums then run near 2 sum(amp)
+// and a low-amplitude window exceeds 1e-5 * A.
+#ifndef TG_MAP_SIGNED
+#define TG_MAP_SIGNED 1
+#endif
+
 namespace tg {
 
 constexpr uint64_t kSeedMul = 0x9E3779B97F4A7C15ULL;  // lattice.hpp:47
@@ -117,44 +131,49 @@ __device__ __forceinline__ float height_scaled(uint64_t packed) {
 // Map-path corner height from the top word of fmix64 only.  The final
 // xorshift (z ^= z >> 33) touches only the low word, and the second multiply
 // needs only its high word (mul.hi of the low words plus both cross terms).
-// With u = that word, corner_height = (u + frac) * 2^-31 - 1, frac in [0, 1).
-// The kernels fold the constant part of every octave (-amp after the scale)
-// into one per-pixel offset (FbmArgs::hoff), which is exact because every
-// zero-gradient / generic cell is an affine blend of its corner heights
-// (weights summing to 1).  The hash itself and tg_lattice_height_f32 stay
-// bit-exact; map heights are checked against the north star's 1e-5 tolerance.
+//
+// Signed form (TG_MAP_SIGNED=1, default).  Map-path keys carry a +2^63 bias
+// (kMapKeyBias, added to seed*K1 by the host planner, so every key the
+// kernels derive from it carries it): with hi' = hi ^ 2^31,
+//   * the xorshifts read lo ^= (hi' >> 1) ^ 2^30 — the same value, the 2^30
+//     riding free in the 3-input LOP3;
+//   * the first multiply's high word comes out as hi1 + 2^31 (the cross term
+//     hi' * C1lo = hi * C1lo + 2^31, C1lo odd), i.e. the flipped hi1' again;
+//   * the last multiply's top word likewise comes out as t + 2^31 = t ^ 2^31.
+// Read as int32, t ^ 2^31 = floor(corner_height * 2^31): the map height is
+// float(int32) * 2^-31 with no per-octave offset and no extra instruction, so
+// fp32 partial sums stay at the magnitude of the map itself and the absolute
+// error scales with each window's own amplitude (tests/test_gpu_fullshape.py
+// checks 1e-5 * A in every 64 x 64 window).  Lanes xor'ed into map-path keys
+// (Perlin / generic gradients, OpenSimplex) carry the same bias (kMapLane).
+//
+// Unsigned form (TG_MAP_SIGNED=0): u = the top word, corner_height =
+// (u + frac) * 2^-31 - 1; the -1 of every octave folds into one per-pixel
+// offset (FbmArgs::hoff), so partial sums run near 2 sum(amp) and a
+// low-amplitude window exceeds 1e-5 * A (round 1).
+#if TG_MAP_HEIGHT_HI && TG_MAP_SIGNED
+constexpr uint64_t kMapKeyBias = 0x8000000000000000ULL;
+constexpr uint32_t kXsBias = 0x40000000u;  // (2^31 >> 1) carried by the xorshift
+#else
+constexpr uint64_t kMapKeyBias = 0;
+constexpr uint32_t kXsBias = 0;
+#endif
+constexpr uint64_t kMapLane(uint64_t lane) { return lane ^ kMapKeyBias; }
+
+#define TG_TOP_WORD(out, l, h)                                                         \
+    asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"                     \
+        "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"  \
+        : "=r"(out)                                                                   \
+        : "r"(l), "r"(h))
+
 __device__ __forceinline__ uint32_t hash_top_word(uint64_t p) {
     uint32_t lo = static_cast<uint32_t>(p), hi = static_cast<uint32_t>(p >> 32);
-    lo ^= hi >> 1;
+    lo ^= (hi >> 1) ^ kXsBias;
     TG_MUL64(lo, hi, 0xED558CCD, 0xFF51AFD7);
-    lo ^= hi >> 1;
+    lo ^= (hi >> 1) ^ kXsBias;
     uint32_t t;
-    asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
-        "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
-        : "=r"(t)
-        : "r"(lo), "r"(hi));
+    TG_TOP_WORD(t, lo, hi);
     return t;
-}
-
-// Four independent keys in lock step (see height_scaled4).
-__device__ __forceinline__ void hash_top_word4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3,
-                                               uint32_t (&out)[4]) {
-    uint32_t l[4] = {static_cast<uint32_t>(p0), static_cast<uint32_t>(p1), static_cast<uint32_t>(p2),
-                     static_cast<uint32_t>(p3)};
-    uint32_t h[4] = {static_cast<uint32_t>(p0 >> 32), static_cast<uint32_t>(p1 >> 32),
-                     static_cast<uint32_t>(p2 >> 32), static_cast<uint32_t>(p3 >> 32)};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) TG_MUL64(l[i], h[i], 0xED558CCD, 0xFF51AFD7);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) l[i] ^= h[i] >> 1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
-            "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
-            : "=r"(out[i])
-            : "r"(l[i]), "r"(h[i]));
 }
 
 // N independent keys in lock step (N-way instruction-level parallelism).
@@ -167,35 +186,40 @@ __device__ __forceinline__ void hash_top_wordN(const uint64_t (&p)[N], uint32_t 
         h[i] = static_cast<uint32_t>(p[i] >> 32);
     }
 #pragma unroll
-    for (int i = 0; i < N; ++i) l[i] ^= h[i] >> 1;
+    for (int i = 0; i < N; ++i) l[i] ^= (h[i] >> 1) ^ kXsBias;
 #pragma unroll
     for (int i = 0; i < N; ++i) TG_MUL64(l[i], h[i], 0xED558CCD, 0xFF51AFD7);
 #pragma unroll
-    for (int i = 0; i < N; ++i) l[i] ^= h[i] >> 1;
+    for (int i = 0; i < N; ++i) l[i] ^= (h[i] >> 1) ^ kXsBias;
 #pragma unroll
-    for (int i = 0; i < N; ++i)
-        asm("{\n\t.reg .b32 q;\n\tmul.hi.u32 q, %1, 0x1A85EC53;\n\t"
-            "mad.lo.u32 q, %2, 0x1A85EC53, q;\n\tmad.lo.u32 %0, %1, 0xC4CEB9FE, q;\n\t}"
-            : "=r"(out[i])
-            : "r"(l[i]), "r"(h[i]));
+    for (int i = 0; i < N; ++i) TG_TOP_WORD(out[i], l[i], h[i]);
+}
+
+// Four independent keys in lock step (see height_scaled4).
+__device__ __forceinline__ void hash_top_word4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3,
+                                               uint32_t (&out)[4]) {
+    const uint64_t p[4] = {p0, p1, p2, p3};
+    hash_top_wordN<4>(p, out);
 }
 
 // The height representation of the map kernels: the corner height is
-// map_height(p) * kMapScale - kMapOffsetUnits (the second term folded into
-// FbmArgs::hoff = -sum(amp), scaled by kMapOffsetUnits in the kernels).
-//   TG_MAP_HEIGHT_HI=1 (default): f = float(u) (one I2FP), height =
-//     f * 2^-31 - 1, |error| <= 2^-24.  10 instructions per key.  (Building
-//     f in [1, 2) from u's high 23 bits with one integer LEA.HI instead
-//     measured the same.)
+// map_height(p) * kMapScale - kMapOffsetUnits (the second term, unsigned form
+// only, folded into FbmArgs::hoff = -sum(amp)).
+//   TG_MAP_HEIGHT_HI=1 (default): one I2FP of the top word, |error| <= 2^-24,
+//     10 instructions per key (signed: float(int32) * 2^-31).
 //   TG_MAP_HEIGHT_HI=0: the exactly rounded height_scaled path, 14 per key.
-#ifndef TG_MAP_HEIGHT_HI
-#define TG_MAP_HEIGHT_HI 1
-#endif
+
 #if TG_MAP_HEIGHT_HI
 constexpr float kMapScale = 0x1p-31f;
+#if TG_MAP_SIGNED
+constexpr float kMapOffsetUnits = 0.0f;
+__device__ __forceinline__ float top_word_height(uint32_t t) { return static_cast<float>(static_cast<int32_t>(t)); }
+constexpr bool kMapOffset = false;
+#else
 constexpr float kMapOffsetUnits = 1.0f;
 __device__ __forceinline__ float top_word_height(uint32_t t) { return static_cast<float>(t); }
 constexpr bool kMapOffset = true;
+#endif
 __device__ __forceinline__ float map_height(uint64_t p) { return top_word_height(hash_top_word(p)); }
 template <int N>
 __device__ __forceinline__ void map_heightN(const uint64_t (&p)[N], float (&o)[N]) {

@@ -32,7 +32,7 @@ constexpr double kSquish = 0.366025403784438646763723170753;    // (sqrt(3) - 1)
 // (the final fmix64 xorshift leaves the high word alone).
 __device__ __forceinline__ uint32_t grad_index(uint64_t base, int64_t xsv, int64_t ysv) {
     uint32_t lo, hi;
-    mix64_pre(pack_xy(base, xsv, ysv) ^ kSimplexLane, lo, hi);
+    mix64_pre(pack_xy(base, xsv, ysv) ^ kMapLane(kSimplexLane), lo, hi);
     return hi >> 29;
 }
 

@@ -153,7 +153,8 @@ def terrain_stats(band: Band, backend, comm: Comm, sizes: Sequence[int], lags: S
     for s in sizes:
         if band.local_y0 % s != 0 or (band.rows % s != 0 and not band.is_last):
             raise ValidationError("terrain_stats: band starts/ends must be multiples of every box size")
-    if lags and max(lags) > band.below and not band.is_last:
+    # vertical pairs need max(lags) rows below the band, or every row left in the terrain
+    if lags and max(lags) > band.below and band.below < band.height - (band.local_y0 + band.rows):
         raise ValidationError("terrain_stats: a variogram lag exceeds the band's regenerated lookahead "
                               "(plan_band max_lag)")
     backend.generate(band)
