@@ -352,7 +352,7 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
             if (tile_terms) {
                 const int q = a->ngroup[tg::kGBlkT];
                 a->oct[o].cslot = q;
-                a->blkt[q] = {d.shift, d.ncx - 1, d.lut_off, d.inv_ppc};
+                a->blkt[q] = {nullptr, d.shift, d.ncx - 1, d.ppc - 1, d.inv_ppc};  // sd: below
             }
             push(tile_terms ? tg::kGBlkT : tg::kGBlk8);
         }
@@ -401,6 +401,8 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
     }
     a->lut = tg::row_lut(order_of(c));
     if (!a->lut) return fail(TG_EDEVICE, "row LUT allocation failed");
+    for (int q = 0; q < a->ngroup[tg::kGBlkT]; ++q)  // (S, S - x) plane of row_lut at [ppc]
+        a->blkt[q].sd = reinterpret_cast<const float2*>(a->lut + tg::kLutN4 + tg::kLutN4 / 2) + (a->blkt[q].mask + 1);
     return TG_OK;
 }
 

@@ -231,8 +231,8 @@ constexpr size_t smem_grid_end() {
     return (LEAN ? 0 : sizeof(TabSlot) * kTabSlots) + sizeof(float) * Traits<KIND>::kCh * kGridCap;
 }
 // floats: Cw[2][128], C1[2][128], Rw[4][64], R1[4][64], then the kGBlkT
-// octaves' cell parameters (h00, dx, dy, a) x 8 cells per slot
-constexpr int kFeat = 4 * 256 + 4 * 8 * kMaxCellSlots;
+// octaves' cell coefficients: column float4 x 8 cells per slot, row float2 x 8
+constexpr int kFeat = 4 * 256 + 6 * 8 * kMaxCellSlots;
 template <int KIND, bool LEAN>
 constexpr size_t smem_bytes() {
     return smem_grid_end<KIND, LEAN>() + (KIND == kZgPaper ? sizeof(float) * kFeat : 0);
@@ -478,17 +478,25 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const OctDev& od = args.oct[args.group[kGProCoarse][q]];
         const int cy = (lane * od.cdiv) >> 16, cx = lane - cy * od.ncx;  // lane / ncx (lane < 32, ncx <= 32)
         if (KIND == kZgPaper && kRPT == 8 && od.cslot >= 0) {
-            // kGBlkT octave: the cells' (h00, dx, dy, a) x amp straight from
-            // the lanes' corners (lane = cy * ncx + cx), no grid
+            // kGBlkT octave: per cell (cx, cy) of the tile, the coefficients
+            // of its column and row terms (see the per-tile block octaves
+            // below) straight from the lanes' corners (lane = cy * ncx + cx):
+            //   column  (h00, dx, a*yc, a/ppc),  row  (dy + a*xc, a/ppc)
+            // with (xc, yc) the cell-local coordinate of the tile's pixel (0, 0).
             float h = map_height(pack_xy(seed_key + od.oct_key, (tx0 >> od.shift) + cx, (ty0 >> od.shift) + cy));
             h *= od.amp * kMapScale;
             const float h10 = __shfl_down_sync(0xffffffffu, h, 1);
             const float h01 = __shfl_down_sync(0xffffffffu, h, od.ncx);
             const float h11 = __shfl_down_sync(0xffffffffu, h, od.ncx + 1);
             if (cx < od.ncx - 1 && cy < od.ncy - 1) {
-                float4* cp = reinterpret_cast<float4*>(smem_raw + smem_grid_end<KIND, LEAN>()) + 256;
-                const float dy = h01 - h;
-                cp[od.cslot * 8 + cy * (od.ncx - 1) + cx] = make_float4(h, h10 - h, dy, (h11 - h10) - dy);
+                const int mask = od.ppc - 1;
+                const float xc = (static_cast<float>((static_cast<int>(tx0) & mask) - (cx << od.shift)) + 0.5f) * od.inv_ppc;
+                const float yc = (static_cast<float>((static_cast<int>(ty0) & mask) - (cy << od.shift)) + 0.5f) * od.inv_ppc;
+                const float dy = h01 - h, a = (h11 - h10) - dy, ai = a * od.inv_ppc;
+                float* base = reinterpret_cast<float*>(smem_raw + smem_grid_end<KIND, LEAN>()) + 1024;
+                const int cell = od.cslot * 8 + cy * (od.ncx - 1) + cx;
+                reinterpret_cast<float4*>(base)[cell] = make_float4(h, h10 - h, a * yc, ai);
+                reinterpret_cast<float2*>(base + 4 * 8 * kMaxCellSlots)[cell] = make_float2(fmaf(a, xc, dy), ai);
             }
         } else if (lane < od.ncx * od.ncy) {
             float d[CH];
@@ -645,33 +653,32 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 // ppc-32 cell rows, threads 128-255 the row entries of
                 // Y = tid % 64 for two ppc-32 cell columns; above ppc 32 the
                 // two entries share their cell, so the term is computed once.
-                const float4* cpar = reinterpret_cast<const float4*>(feat) + 256;
+                // Per octave and entry: one LUT load, one shared load of the
+                // cell's coefficients (coarse prologue), 2-3 FFMA.
+                const float4* colp = reinterpret_cast<const float4*>(feat + 1024);
+                const float2* rowp = reinterpret_cast<const float2*>(feat + 1024 + 4 * 8 * kMaxCellSlots);
                 const int tlx = static_cast<int>(tx0), tly = static_cast<int>(ty0);  // (& mask: low bits)
                 const int nq = args.ngroup[kGBlkT];
                 if (tid < 128) {
                     const int X = tid;
                     float cwA = 0.f, cwB = 0.f, c1A = 0.f, c1B = 0.f;
-                    for (int q = 0; q < nq; ++q) {
-                        const BlkTDev b = args.blkt[q];
-                        const int sh = b.shift, mask = (1 << sh) - 1;
-                        const int tmy = tly & mask;
-                        const float4* cq = cpar + q * 8;
-                        const float4 e = __ldg(args.lut + b.lut_off + ((tlx + X) & mask));  // x, S, S - x
-                        const int cx = X >> sh;
-                        const float4 cp = cq[cx];  // h00, dx, dy, a
-                        const float yc = (static_cast<float>(tmy) + 0.5f) * b.inv;
-                        const float tA = fmaf(cp.w * yc, e.z, fmaf(e.y, cp.y, cp.x));
-                        const float uA = cp.w * b.inv;
+#pragma unroll
+                    for (int q = 0; q < kMaxCellSlots; ++q) {
+                        if (q >= nq) break;
+                        const BlkTDev& b = args.blkt[q];
+                        const int sh = b.shift;
+                        const float2 e = __ldg(b.sd + ((tlx + X) & b.mask));  // S, S - x
+                        const float4 cp = colp[q * 8 + (X >> sh)];
+                        const float tA = fmaf(cp.z, e.y, fmaf(e.x, cp.y, cp.x));
                         cwA += tA;
-                        c1A = fmaf(uA, e.z, c1A);
+                        c1A = fmaf(cp.w, e.y, c1A);
                         if (sh == 5) {  // second ppc-32 cell row
-                            const float4 cpB = cq[b.ncx1 + cx];
-                            const float ycB = (static_cast<float>(tmy - 32) + 0.5f) * b.inv;
-                            cwB += fmaf(cpB.w * ycB, e.z, fmaf(e.y, cpB.y, cpB.x));
-                            c1B = fmaf(cpB.w * b.inv, e.z, c1B);
+                            const float4 cpB = colp[q * 8 + b.ncx1 + (X >> 5)];
+                            cwB += fmaf(cpB.z, e.y, fmaf(e.x, cpB.y, cpB.x));
+                            c1B = fmaf(cpB.w, e.y, c1B);
                         } else {
                             cwB += tA;
-                            c1B = fmaf(uA, e.z, c1B);
+                            c1B = fmaf(cp.w, e.y, c1B);
                         }
                     }
                     feat[X] = cwA;
@@ -681,26 +688,23 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 } else {
                     const int u = tid - 128, Y = u & 63, ccA = (u >> 6) * 2;
                     float rwA = 0.f, rwB = 0.f, r1A = 0.f, r1B = 0.f;
-                    for (int q = 0; q < nq; ++q) {
-                        const BlkTDev b = args.blkt[q];
-                        const int sh = b.shift, mask = (1 << sh) - 1;
-                        const int tmx = tlx & mask;
-                        const float4* cq = cpar + q * 8;
-                        const float sy = __ldg(args.lut + b.lut_off + ((tly + Y) & mask)).y;
+#pragma unroll
+                    for (int q = 0; q < kMaxCellSlots; ++q) {
+                        if (q >= nq) break;
+                        const BlkTDev& b = args.blkt[q];
+                        const int sh = b.shift;
+                        const float sy = __ldg(b.sd + ((tly + Y) & b.mask)).x;
                         const int cr = Y >> sh, cc = (ccA << 5) >> sh;
-                        const float4 cp = cq[cr * b.ncx1 + cc];
-                        const float xc = (static_cast<float>(tmx - (cc << sh)) + 0.5f) * b.inv;
-                        const float tA = fmaf(cp.w, xc, cp.z), uA = cp.w * b.inv;
-                        rwA = fmaf(sy, tA, rwA);
-                        r1A = fmaf(uA, sy, r1A);
+                        const float2 rp = rowp[q * 8 + cr * b.ncx1 + cc];
+                        rwA = fmaf(sy, rp.x, rwA);
+                        r1A = fmaf(rp.y, sy, r1A);
                         if (sh == 5) {  // second ppc-32 cell column
-                            const float4 cpB = cq[cr * b.ncx1 + cc + 1];
-                            const float xcB = (static_cast<float>(tmx - ((cc + 1) << sh)) + 0.5f) * b.inv;
-                            rwB = fmaf(sy, fmaf(cpB.w, xcB, cpB.z), rwB);
-                            r1B = fmaf(cpB.w * b.inv, sy, r1B);
+                            const float2 rpB = rowp[q * 8 + cr * b.ncx1 + cc + 1];
+                            rwB = fmaf(sy, rpB.x, rwB);
+                            r1B = fmaf(rpB.y, sy, r1B);
                         } else {
-                            rwB = fmaf(sy, tA, rwB);
-                            r1B = fmaf(uA, sy, r1B);
+                            rwB = fmaf(sy, rp.x, rwB);
+                            r1B = fmaf(rp.y, sy, r1B);
                         }
                     }
                     feat[512 + ccA * 64 + Y] = rwA;

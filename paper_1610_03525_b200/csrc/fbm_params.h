@@ -113,8 +113,9 @@ constexpr int kFineSlots = 5;
 // kGBlkT octave q (ppc = 2^shift >= 32): per-slot constants of the per-tile
 // column / row terms, indexed by list position (cell parameters at slot q).
 struct BlkTDev {
-    int32_t shift, ncx1, lut_off;  // log2 ppc, cell columns per tile (ncx - 1), row LUT offset
-    float inv;                     // 1 / ppc
+    const float2* sd;          // (S, S - x) row LUT of this ppc (row_lut's float2 plane at [ppc])
+    int32_t shift, ncx1, mask;  // log2 ppc, cell columns per tile (ncx - 1), ppc - 1
+    float inv;                  // 1 / ppc
 };
 
 struct FbmArgs {

@@ -51,7 +51,8 @@ cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uin
 // once per device in fp64 and rounded to fp32: entry (x, S(x), S(x)-x, x*S(x))
 // at [ppc - 1 + r], followed by two planar copies, S(x) at float [ppc + r] and
 // S(x) - x at float [kLutN4 + ppc + r] past the kLutN4-entry float4 block, so
-// that 4 consecutive rows / columns are one aligned 16-byte load.
+// that 4 consecutive rows / columns are one aligned 16-byte load, then the
+// pairs (S(x), S(x) - x) as float2 at [ppc + r] (one 8-byte load per column).
 // Immutable after creation, so concurrent callers share it (like the
 // reference's thread-local cached_row_lut, kernels2d.hpp:246-259).
 const float4* row_lut(int order) {
@@ -63,8 +64,9 @@ const float4* row_lut(int order) {
     const int oi = order == 5 ? 1 : 0;
     std::lock_guard<std::mutex> lock(mu);
     if (luts[dev][oi]) return luts[dev][oi];
-    std::vector<float4> h(static_cast<size_t>(kLutN4 + 2 * kLutN4 / 4), make_float4(0.f, 0.f, 0.f, 0.f));
+    std::vector<float4> h(static_cast<size_t>(kLutN4 + 2 * kLutN4 / 4 + kLutN4 / 2), make_float4(0.f, 0.f, 0.f, 0.f));
     float* planes = reinterpret_cast<float*>(h.data() + kLutN4);
+    float2* sd = reinterpret_cast<float2*>(h.data() + kLutN4 + kLutN4 / 2);  // (S, S - x) at [ppc + r]
     for (int k = 0; k <= kLutLog2Max; ++k) {
         const int ppc = 1 << k;
         for (int r = 0; r < ppc; ++r) {
@@ -74,6 +76,7 @@ const float4* row_lut(int order) {
                                                               static_cast<float>(sv - x), static_cast<float>(x * sv));
             planes[ppc + r] = static_cast<float>(sv);
             planes[kLutN4 + ppc + r] = static_cast<float>(sv - x);
+            sd[ppc + r] = make_float2(static_cast<float>(sv), static_cast<float>(sv - x));
         }
     }
     float4* d = nullptr;
