@@ -385,6 +385,21 @@ int build_args(const tg_fbm_config* c, int64_t ox, int64_t oy, int64_t width, in
         }
         a->ngroup[tg::kGProFine] = n;
     }
+    // zg paper ppc 4 / 8 / 16 block octaves: evaluated by their fine slot with
+    // compile-time shapes (fbm2d.cu blk_slot) instead of the kGBlk4 / kGBlk8 lists
+    if (paper && tg::fbm2d_tile_h() == 64) {
+        for (int sh = 2; sh <= 4; ++sh) {
+            tg::FineDev& f = a->fine[sh];
+            if (f.goff < 0) continue;
+            const int g = sh == 2 ? tg::kGBlk4 : tg::kGBlk8;
+            int n = 0;
+            for (int q = 0; q < a->ngroup[g]; ++q) {
+                if (a->group[g][q] == f.oct) f.blk = 1;
+                else a->group[g][n++] = a->group[g][q];
+            }
+            a->ngroup[g] = n;
+        }
+    }
     // tile-store staging over the ppc-1 grid (plan_octaves puts it at offset 0)
     a->stage_pairs = 0;
     if (tg::fbm2d_tile_h() == 64) {

@@ -257,6 +257,19 @@ struct Ppc2W {
     }
 };
 
+// S(x) and S(x) - x at the ppc-4 sample positions x = (2i + 1)/8, i = 0..3
+// (smoothstep3/5, kernels2d.hpp:26-38), exact in fp32 (the row LUT's fp64
+// values rounded once: every one of them is a dyadic rational with < 24 bits).
+template <int ORDER>
+struct Ppc4S {
+    static constexpr double Sd(int i) {
+        const double x = (2.0 * i + 1.0) / 8.0;
+        return ORDER == 5 ? x * x * x * (10.0 + x * (6.0 * x - 15.0)) : x * x * (3.0 - 2.0 * x);
+    }
+    static constexpr float S(int i) { return static_cast<float>(Sd(i)); }
+    static constexpr float D(int i) { return static_cast<float>(Sd(i) - (2.0 * i + 1.0) / 8.0); }
+};
+
 // q*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
 // rows r = 0..8 of a 5-wide corner strip: x = y = 0.5 makes every zero-
 // gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners
@@ -520,9 +533,10 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         const uint64_t p0 = seed_key + fd.key0 + static_cast<uint64_t>(blockIdx.x) * fd.kx +
                             static_cast<uint64_t>(blockIdx.y) * fd.ky;
         float* g = grid + fd.goff;
-        if constexpr (kZg && SH == 1) {
-            // the ppc-2 grid is stored amplitude-scaled (its corner blends read it as is)
-            const float sc = args.oct[fd.oct].amp * kMapScale;
+        if constexpr (kZg && (SH == 1 || (KIND == kZgPaper && SH >= 2))) {
+            // the ppc-2 grid (and the slot-evaluated ppc 4 / 8 / 16 grids) are
+            // stored amplitude-scaled (their evaluation reads them as is)
+            const float sc = (SH == 1 || fd.blk) ? args.oct[fd.oct].amp * kMapScale : 1.0f;
             fine_grid<SH, CH, true>(g, fd.pitch, p0, warp, lane, tid, fd.rot, grid_value, args.oct[fd.oct], sc);
         } else {
             fine_grid<SH, CH>(g, fd.pitch, p0, warp, lane, tid, fd.rot, grid_value, args.oct[fd.oct]);
@@ -738,6 +752,43 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 }
             }
         }
+        // ppc 8 / 16 from their fine slots (compile-time shape, amplitude-
+        // scaled grids): the same separated-form terms as the list below.
+        // Tiles are 128 x 64 aligned, so the thread's block starts at cell
+        // offset (c0 & (PPC - 1), r0 & (PPC - 1)).
+        auto blk_slot = [&](auto sh_c) {
+            constexpr int SH = decltype(sh_c)::value, PPC = 1 << SH;
+            constexpr float inv = 1.0f / PPC;
+            const FineDev& fd = args.fine[SH];
+            if ((TG_SKIP & 4) || !fd.blk) return;
+            const int mx = c0 & (PPC - 1), my = r0 & (PPC - 1);
+            const float* g = grid + fd.goff + (r0 >> SH) * fd.pitch + (c0 >> SH);
+            const float h00 = g[0], h10 = g[1], h01 = g[fd.pitch], h11 = g[fd.pitch + 1];
+            const float dx = h10 - h00, dy = h01 - h00, a = (h11 - h10) - dy;
+            const float x0 = (static_cast<float>(mx) + 0.5f) * inv, y0 = (static_cast<float>(my) + 0.5f) * inv;
+            const float4 sx = __ldg(reinterpret_cast<const float4*>(lutS + PPC + mx));
+            const float4 dd = __ldg(reinterpret_cast<const float4*>(lutD + PPC + mx));
+            const float sxa[4] = {sx.x, sx.y, sx.z, sx.w}, dda[4] = {dd.x, dd.y, dd.z, dd.w};
+            const float ay0 = a * y0, ad = a * inv, k0 = fmaf(a, x0, dy);
+            hsum += h00;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                C0[j] = fmaf(dda[j], ay0, fmaf(sxa[j], dx, C0[j]));
+                C1[j] = fmaf(dda[j], ad, C1[j]);
+            }
+#pragma unroll
+            for (int r4 = 0; r4 < kRPT; r4 += 4) {
+                const float4 sy = __ldg(reinterpret_cast<const float4*>(lutS + PPC + my + r4));
+                const float sya[4] = {sy.x, sy.y, sy.z, sy.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    R0[r4 + i] = fmaf(sya[i], k0, R0[r4 + i]);
+                    R1[r4 + i] = fmaf(sya[i], ad, R1[r4 + i]);
+                }
+            }
+        };
+        blk_slot(std::integral_constant<int, 4>{});
+        blk_slot(std::integral_constant<int, 3>{});
         for (int q = 0; q < TG_NG(kGBlk8, 4); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk8][q]];
             const int sh = od.shift, mask = od.ppc - 1;
@@ -778,6 +829,37 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
         // added to rows 4-7 only.
         float D0[4] = {0.f, 0.f, 0.f, 0.f}, D1[4] = {0.f, 0.f, 0.f, 0.f};
         static_assert(kRPT == 8, "ppc-4 blocks assume 8 rows per thread (two cell rows)");
+        // slot-evaluated ppc 4 (amplitude-scaled grid, x = 1/8 + c/4: S(x)
+        // and S(x) - x as compile-time constants)
+        if (!(TG_SKIP & 16) && args.fine[2].blk) {
+            const FineDev& fd = args.fine[2];
+            const int pitch = fd.pitch;
+            const float* g = grid + fd.goff + (r0 >> 2) * pitch + (c0 >> 2);
+            const float a0 = g[0], a1 = g[1], b0 = g[pitch], b1 = g[pitch + 1];
+            const float e0 = g[2 * pitch], e1 = g[2 * pitch + 1];
+            const float dyA = b0 - a0, aA = (b1 - a1) - dyA, dxA = a1 - a0;
+            const float dyB = e0 - b0, aB = (e1 - b1) - dyB, dxB = b1 - b0;
+            const float qA = 0.25f * aA, qB = 0.25f * aB;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float sj = Ppc4S<ORDER>::S(j), dj = Ppc4S<ORDER>::D(j);
+                const float cA = fmaf(0.125f * aA, dj, fmaf(sj, dxA, a0));
+                const float cB = fmaf(-0.875f * aB, dj, fmaf(sj, dxB, b0));
+                C0[j] += cA;
+                D0[j] += cB - cA;
+                C1[j] = fmaf(qA, dj, C1[j]);
+                D1[j] = fmaf(qB - qA, dj, D1[j]);
+            }
+            const float kA = fmaf(0.125f, aA, dyA), kB = fmaf(0.125f, aB, dyB);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float sr = Ppc4S<ORDER>::S(r);
+                R0[r] = fmaf(sr, kA, R0[r]);
+                R1[r] = fmaf(sr, qA, R1[r]);
+                R0[r + 4] = fmaf(sr, kB, R0[r + 4]);
+                R1[r + 4] = fmaf(sr, qB, R1[r + 4]);
+            }
+        }
         for (int q = 0; q < TG_NG(kGBlk4, 16); ++q) {
             const OctDev& od = args.oct[args.group[kGBlk4][q]];
             const float4* L = args.lut + od.lut_off;  // 4 entries: x = 1/8, 3/8, 5/8, 7/8

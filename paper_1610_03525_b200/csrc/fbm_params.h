@@ -107,6 +107,9 @@ struct FineDev {
     int32_t goff, pitch;    // grid offset / row stride (floats)
     int32_t rot;            // starting warp (list position & 7)
     int32_t oct;            // octave index (corner data of Perlin / generic grids)
+    int32_t blk;            // zg paper ppc 4 / 8 / 16: grid stored amplitude-scaled and the
+                            // octave evaluated by its slot with compile-time shape (not listed)
+    int32_t pad_;
 };
 constexpr int kFineSlots = 5;
 
