@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -830,10 +831,12 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
             long_x = long_x || (!pad && h > kApron);
         }
         const int vi = (n - 1) / 2;
-        xt[long_x ? 1 : 0][vi]<<<static_cast<unsigned>(xblocks), kVgThreads, smem, s>>>(
+        // TG_VG_AXES (timing experiments only): 1 = x pass only, 2 = y pass only
+        static const int axes = getenv("TG_VG_AXES") ? atoi(getenv("TG_VG_AXES")) : 3;
+        if (axes & 1) xt[long_x ? 1 : 0][vi]<<<static_cast<unsigned>(xblocks), kVgThreads, smem, s>>>(
             dev_map, width, ld, pair_rows, Lx, nseg, seg_cap, sums + 2 * l0);
         if ((e = cudaGetLastError()) != cudaSuccess) break;
-        yt[vec ? 1 : 0][vi]<<<static_cast<unsigned>(yblocks), kVgThreads, 0, sy>>>(dev_map, width, height, ld,
+        if (axes & 2) yt[vec ? 1 : 0][vi]<<<static_cast<unsigned>(yblocks), kVgThreads, 0, sy>>>(dev_map, width, height, ld,
                                                                                   pair_rows, Ly, sums + 2 * l0);
         e = cudaGetLastError();
     }
