@@ -50,7 +50,18 @@ enum tg_method {
     TG_METHOD_GENERIC = 2,
     TG_METHOD_PERLIN3 = 3,
     TG_METHOD_PERLIN5 = 4,
-    TG_METHOD_OPENSIMPLEX = 5
+    TG_METHOD_OPENSIMPLEX = 5,
+    /* Classic permutation-table Perlin gradient noise (BASELINE config 3; the
+     * reference deliberately hashes gradient angles instead).
+     * New, parity unpinned (restated oracle only).  Per seed: s = seed*K1;
+     * P = the permutation of 0..255 sorting key_i = mix(s ^ i*TG_PERM_KI ^
+     * TG_LANE_PERM) ascending (ties by i); per octave o an offset
+     * t = mix((s + o*K2) ^ TG_LANE_PERM), (ox, oy) = (t & 255, (t >> 8) & 255);
+     * corner (ix, iy) takes gradient k = P[(P[(ix + ox) & 255] + iy + oy) & 255]
+     * & 7 of the 8 unit vectors at angles k*45 degrees; the cell is the
+     * reference's Perlin cell (kernels2d.hpp:163-173) with the fade of
+     * `smoothstep` (default S5, "improved noise"). */
+    TG_METHOD_PERLIN_PERM = 6
 };
 
 /* Lifted caps: the reference caps resolution and extent at
@@ -65,6 +76,9 @@ enum tg_method {
 #define TG_LANE_MAGNITUDE 0xE7037ED1A0B428DBULL
 /* OpenSimplex gradient-selection lane (new): index = mix(pack ^ lane) >> 61. */
 #define TG_LANE_SIMPLEX 0x8EBC6AF09C88C6E3ULL
+/* Permutation-table Perlin lanes (new): table keys and octave offsets. */
+#define TG_LANE_PERM 0x5851F42D4C957F2DULL
+#define TG_PERM_KI 0xD1B54A32D192ED03ULL
 /* 3D key extension (new): pack3 = pack2 + (u64)iz * K5,
  * so iz = 0 reproduces the 2D lattice exactly. */
 #define TG_PACK_K5 0xA24BAED4963EE407ULL

@@ -64,8 +64,9 @@ inline void check(int status) {
 namespace fbm {
 
 // fbm.hpp:27, plus opensimplex (the paper's third baseline; absent from the
-// reference)
-enum class Method { zg_paper, zg_separable, generic, perlin3, perlin5, opensimplex };
+// reference) and the classic permutation-table Perlin (BASELINE
+// config 3; the reference hashes gradient angles instead)
+enum class Method { zg_paper, zg_separable, generic, perlin3, perlin5, opensimplex, perlin_perm };
 
 inline const char* method_name(Method m) {  // fbm.hpp:29-38
     switch (m) {
@@ -75,6 +76,7 @@ inline const char* method_name(Method m) {  // fbm.hpp:29-38
         case Method::perlin3: return "perlin3";
         case Method::perlin5: return "perlin5";
         case Method::opensimplex: return "opensimplex";
+        case Method::perlin_perm: return "perlin_perm";
     }
     return "unknown";
 }
@@ -86,6 +88,7 @@ inline std::optional<Method> parse_method(std::string_view name) {  // fbm.hpp:4
     if (name == "perlin3" || name == "perlin") return Method::perlin3;
     if (name == "perlin5") return Method::perlin5;
     if (name == "opensimplex") return Method::opensimplex;
+    if (name == "perlin_perm") return Method::perlin_perm;
     return std::nullopt;
 }
 
@@ -109,7 +112,7 @@ struct FbmConfig {  // fbm.hpp:49-89
     }
     int smoothstep_order() const {
         if (smoothstep) return smoothstep;
-        return method == Method::perlin5 ? 5 : 3;
+        return method == Method::perlin5 || method == Method::perlin_perm ? 5 : 3;
     }
     tg_fbm_config to_c() const {
         tg_fbm_config c{};

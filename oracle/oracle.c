@@ -224,14 +224,14 @@ int or_validate(const tg_fbm_config* c) {
     if (c->has_gradient_weight && (!(c->gradient_weight >= 0.0) || !isfinite(c->gradient_weight)))
         return TG_EVALIDATION;
     if (c->threads < 0 || c->threads > 256) return TG_EVALIDATION;
-    if (c->method < 0 || c->method > TG_METHOD_OPENSIMPLEX) return TG_EVALIDATION;
+    if (c->method < 0 || c->method > TG_METHOD_PERLIN_PERM) return TG_EVALIDATION;
     if (c->smoothstep != 0 && c->smoothstep != 3 && c->smoothstep != 5) return TG_EVALIDATION;
     return TG_OK;
 }
 
 static int order_of(const tg_fbm_config* c) {
     if (c->smoothstep) return c->smoothstep;
-    return c->method == TG_METHOD_PERLIN5 ? 5 : 3; /* fbm.hpp:66-69 */
+    return c->method == TG_METHOD_PERLIN5 || c->method == TG_METHOD_PERLIN_PERM ? 5 : 3; /* fbm.hpp:66-69 */
 }
 
 static double weight_of(const tg_fbm_config* c) {
@@ -270,6 +270,40 @@ typedef struct {
     double h, f, g;
 } corner_t;
 
+/* Permutation-table Perlin (TG_METHOD_PERLIN_PERM, new; definition in
+ * include/polyterrain_b200.h): P sorts the 256 keys mix(s ^ i*KI ^ lane). */
+void or_perm_table(uint64_t seed, uint8_t out[256]) {
+    const uint64_t s = seed * 0x9E3779B97F4A7C15ULL;
+    uint64_t key[256];
+    for (int i = 0; i < 256; ++i) key[i] = or_mix(s ^ ((uint64_t)i * TG_PERM_KI) ^ TG_LANE_PERM);
+    for (int i = 0; i < 256; ++i) {
+        int rank = 0;
+        for (int j = 0; j < 256; ++j) rank += key[j] < key[i] || (key[j] == key[i] && j < i);
+        out[rank] = (uint8_t)i;
+    }
+}
+
+static _Thread_local uint64_t perm_seed_cached;
+static _Thread_local int perm_cached;
+static _Thread_local uint8_t perm_tab[256];
+
+void or_perm_gradient(uint64_t seed, uint32_t oct, int64_t ix, int64_t iy, double out[2]) {
+    static const double R = 0.70710678118654752440;
+    static const double G[8][2] = {{1, 0}, {R, R}, {0, 1}, {-R, R}, {-1, 0}, {-R, -R}, {0, -1}, {R, -R}};
+    if (!perm_cached || perm_seed_cached != seed) {
+        or_perm_table(seed, perm_tab);
+        perm_seed_cached = seed;
+        perm_cached = 1;
+    }
+    const uint64_t s = seed * 0x9E3779B97F4A7C15ULL;
+    const uint64_t t = or_mix((s + (uint64_t)oct * 0xBF58476D1CE4E5B9ULL) ^ TG_LANE_PERM);
+    const int64_t ox = (int64_t)(t & 255), oy = (int64_t)((t >> 8) & 255);
+    const int a = perm_tab[(ix + ox) & 255];
+    const int k = perm_tab[(a + iy + oy) & 255] & 7;
+    out[0] = G[k][0];
+    out[1] = G[k][1];
+}
+
 static corner_t corner_data(const tg_fbm_config* c, int oct, double amp, int64_t ix, int64_t iy,
                             int need_h, int need_grad, int need_unit) {
     corner_t k = {0.0, 0.0, 0.0};
@@ -283,7 +317,10 @@ static corner_t corner_data(const tg_fbm_config* c, int oct, double amp, int64_t
     }
     if (need_unit) {
         double g[2];
-        or_corner_unit_gradient(c->seed, (uint32_t)oct, ix, iy, g);
+        if (c->method == TG_METHOD_PERLIN_PERM)
+            or_perm_gradient(c->seed, (uint32_t)oct, ix, iy, g);
+        else
+            or_corner_unit_gradient(c->seed, (uint32_t)oct, ix, iy, g);
         k.f = amp * g[0];
         k.g = amp * g[1];
     }

@@ -76,6 +76,8 @@ class Oracle:
             "or_generate_mt": (C.c_int, [PCFG, I64, I64, I64, I64, P, I32]),
             "or_sample3d": (C.c_int, [PCFG, P, P, P, I64, P]),
             "or_cell3": (F64, [P, F64, F64, F64, C.c_int]),
+            "or_perm_table": (None, [U64, P]),
+            "or_perm_gradient": (None, [U64, C.c_uint32, I64, I64, P]),
             "or_normalize": (C.c_int, [P, I64, C.POINTER(F64), C.POINTER(F64), C.POINTER(C.c_int)]),
             "or_upper_median": (F64, [P, I64]),
             "or_coastline_mask": (C.c_int, [P, I64, F64, P, C.POINTER(I64)]),
@@ -157,6 +159,16 @@ class Oracle:
     def cell3(self, h, x: float, y: float, z: float, order: int) -> float:
         hh = np.ascontiguousarray(h, dtype=np.float64)
         return self.lib.or_cell3(_ptr(hh), x, y, z, order)
+
+    def perm_table(self, seed: int) -> np.ndarray:
+        out = np.zeros(256, dtype=np.uint8)
+        self.lib.or_perm_table(seed, _ptr(out))
+        return out
+
+    def perm_gradient(self, seed: int, octave: int, ix: int, iy: int):
+        buf = (C.c_double * 2)()
+        self.lib.or_perm_gradient(seed, octave, ix, iy, buf)
+        return buf[0], buf[1]
 
     def sample(self, cfg: TgFbmConfig, gx, gy) -> np.ndarray:
         x = np.ascontiguousarray(gx, dtype=np.int64)

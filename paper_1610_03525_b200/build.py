@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libpolyterrain_b200.so")
-SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu",
+SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "perm2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu",
            "hostpipe.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

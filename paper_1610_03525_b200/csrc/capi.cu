@@ -66,7 +66,7 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 int order_of(const tg_fbm_config* c) {
     if (c->smoothstep) return c->smoothstep;
-    return c->method == TG_METHOD_PERLIN5 ? 5 : 3;  // fbm.hpp:66-69
+    return c->method == TG_METHOD_PERLIN5 || c->method == TG_METHOD_PERLIN_PERM ? 5 : 3;  // fbm.hpp:66-69
 }
 
 int kind_of(const tg_fbm_config* c) {
@@ -75,6 +75,7 @@ int kind_of(const tg_fbm_config* c) {
         case TG_METHOD_ZG_SEPARABLE: return tg::kZgSeparable;
         case TG_METHOD_GENERIC: return tg::kGeneric;
         case TG_METHOD_OPENSIMPLEX: return tg::kOpenSimplex;
+        case TG_METHOD_PERLIN_PERM: return tg::kPerlinPerm;
         default: return tg::kPerlin;
     }
 }
@@ -238,7 +239,7 @@ int validate_cfg(const tg_fbm_config* c) {
         return fail(TG_EVALIDATION, "fbm config: gradient_weight must be non-negative");
     if (c->threads < 0 || c->threads > 256)
         return fail(TG_EVALIDATION, "fbm config: threads must be in [0, 256]");
-    if (c->method < TG_METHOD_ZG_PAPER || c->method > TG_METHOD_OPENSIMPLEX)
+    if (c->method < TG_METHOD_ZG_PAPER || c->method > TG_METHOD_PERLIN_PERM)
         return fail(TG_EVALIDATION, "fbm config: unknown method");
     if (c->smoothstep != 0 && c->smoothstep != 3 && c->smoothstep != 5)
         return fail(TG_EVALIDATION, "fbm config: smoothstep must be 0, 3 or 5");

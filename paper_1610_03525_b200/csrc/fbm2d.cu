@@ -1534,9 +1534,11 @@ static cudaError_t launch_t(const FbmArgs& a, float* out, cudaStream_t st) {
 int fbm2d_tile_h() { return kTH; }
 
 cudaError_t simplex2d_launch(const FbmArgs& a, float* out, cudaStream_t st);
+cudaError_t perm2d_launch(int order, const FbmArgs& a, float* out, cudaStream_t st);
 
 cudaError_t fbm2d_launch(int kind, int order, const FbmArgs& a, float* out, cudaStream_t st) {
     if (kind == kOpenSimplex) return simplex2d_launch(a, out, st);
+    if (kind == kPerlinPerm) return perm2d_launch(order, a, out, st);
     if (order == 5) {
         switch (kind) {
             case kZgPaper: return launch_t<kZgPaper, 5>(a, out, st);

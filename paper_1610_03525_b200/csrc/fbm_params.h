@@ -21,7 +21,7 @@ enum OctaveClass : int32_t {
     kClsGeneral = 2,  // render_general: u = ((g + 0.5)/R)*freq in fp64 (fbm.hpp:468,474)
 };
 
-enum KernelKind : int32_t { kZgPaper = 0, kZgSeparable = 1, kGeneric = 2, kPerlin = 3, kOpenSimplex = 4 };
+enum KernelKind : int32_t { kZgPaper = 0, kZgSeparable = 1, kGeneric = 2, kPerlin = 3, kOpenSimplex = 4, kPerlinPerm = 5 };
 
 constexpr int kMaxOctaves = 32;
 constexpr int kMaxCellSlots = 10;  // kGBlkT octaves with per-tile cell parameters (8 cells each)

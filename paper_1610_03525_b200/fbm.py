@@ -58,6 +58,7 @@ class Method(enum.IntEnum):
     perlin3 = 3
     perlin5 = 4
     opensimplex = 5  # B200 extension: the paper's third baseline (parity unpinned)
+    perlin_perm = 6  # B200 extension: permutation-table Perlin (BASELINE config 3; parity unpinned)
 
 
 def method_name(m: Method) -> str:  # fbm.hpp:29-38
@@ -68,7 +69,8 @@ def parse_method(name: str) -> Optional[Method]:  # fbm.hpp:40-47
     return {"zg_paper": Method.zg_paper, "zg": Method.zg_paper,
             "zg_separable": Method.zg_separable, "generic": Method.generic,
             "perlin3": Method.perlin3, "perlin": Method.perlin3,
-            "perlin5": Method.perlin5, "opensimplex": Method.opensimplex}.get(name)
+            "perlin5": Method.perlin5, "opensimplex": Method.opensimplex,
+            "perlin_perm": Method.perlin_perm}.get(name)
 
 
 @dataclass
@@ -97,7 +99,7 @@ class FbmConfig:
     def smoothstep_order(self) -> int:  # fbm.hpp:66-69 (+ explicit override)
         if self.smoothstep:
             return self.smoothstep
-        return 5 if self.method == Method.perlin5 else 3
+        return 5 if self.method in (Method.perlin5, Method.perlin_perm) else 3
 
     def to_c(self) -> _abi.TgFbmConfig:
         c = _abi.TgFbmConfig()

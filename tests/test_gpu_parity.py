@@ -579,3 +579,33 @@ def test_back_to_back_launches_keep_stream_order():
             snap = buf.clone()  # a torch kernel reading the output right after
             assert torch.equal(snap.cpu(), refs[it % 3]), it
     torch.cuda.synchronize()
+
+
+# ---- permutation-table Perlin (new; parity unpinned: restated oracle) ---------------
+
+@pytest.mark.parametrize("R,f0,octs,ratio,order", [(256, 2, 6, 2.0, 0), (240, 3, 5, 2.0, 3), (200, 2, 5, 1.7, 5),
+                                                   (512, 8, 9, 2.0, 0)])
+def test_perm_perlin_matches_restated_oracle(oracle, R, f0, octs, ratio, order):
+    c = make_cfg(method=6, seed=31, resolution=R, base_frequency=f0, octaves=octs, frequency_ratio=ratio,
+                 smoothstep=order)
+    check_close(gen(c, 0, 0, R).cpu().numpy(), oracle.generate(c, 0, 0, R), c, f"perm R{R}")
+    # negative origins wrap the table like the oracle's & 255
+    o = -R
+    check_close(gen(c, o, o, R).cpu().numpy(), oracle.generate(c, o, o, R), c, f"perm R{R} negative origin")
+
+
+def test_perm_perlin_region_batch_and_zero():
+    c = make_cfg(method=6, seed=77, resolution=512, base_frequency=4, octaves=7)
+    full = gen(c, 0, 0, 512)
+    assert torch.equal(gen(c, 128, 256, 256), full[256:, 128:384])
+    cz = make_cfg(method=6, seed=77, resolution=512, base_frequency=4, octaves=7, zero_lattice=1)
+    assert torch.count_nonzero(gen(cz, 0, 0, 128)) == 0
+    cfg = pt.FbmConfig(method=pt.Method.perlin_perm, resolution=256, base_frequency=4, octaves=5)
+    seeds = [3, 9, 27]
+    out = torch.empty((3, 256, 256), dtype=torch.float32, device="cuda")
+    pt.generate_batch_device(cfg, seeds, (0, 0), 256, 256, out)
+    for i, s in enumerate(seeds):
+        one = torch.empty((256, 256), dtype=torch.float32, device="cuda")
+        pt.generate_into_device(pt.FbmConfig(method=pt.Method.perlin_perm, seed=s, resolution=256,
+                                             base_frequency=4, octaves=5), (0, 0), 256, one)
+        assert torch.equal(out[i], one)
