@@ -79,7 +79,7 @@ def analysis_pass(lib, ccfg, buf, stream_ptr, world, rank):
     from paper_1610_03525_b200 import _abi
     from paper_1610_03525_b200.shard import Comm, distributed_upper_median
 
-    comm = Comm(device=torch.device("cuda", torch.cuda.current_device()))
+    comm = Comm.nccl(device=torch.device("cuda", torch.cuda.current_device()))
     sizes = [2, 4, 8, 16, 32, 64]
     lags = [1 << i for i in range(12)]
 
@@ -120,6 +120,80 @@ def analysis_pass(lib, ccfg, buf, stream_ptr, world, rank):
     return {"median_coast_boxcount_ms": (t1 - t0) * 1e3, "variogram_ms": (t2 - t1) * 1e3,
             "allreduce_ms": (t3 - t2) * 1e3, "sea_level": sea, "box_counts": counts, "d_box": -slope,
             "note": "per-rank 4096^2 map, second (warm) pass; host wall clock incl. syncs; statistics all-reduced over ranks"}
+
+
+T5, F05, OCT5 = 32768, 32, 16  # config 5: 32768^2, base cell 1024 px (f0 = 32), 16 octaves, zg_paper S5
+
+
+def cfg5_terrain(lib, world: int, rank: int, steps: int = 3, analysis: bool = True):
+    """Config 5 on the N ranks of this job: the 32768^2 terrain in N row bands
+    (strong scaling: the terrain is fixed), each rank generating its band
+    (CUDA events, max over ranks), then the fractal statistics of the whole
+    terrain through the C-ABI driver tg_terrain_stats_band — band regenerated
+    with halo / lookahead rows, radix-select median, coastline + box counts
+    (eps 2..64), variogram over lags 1..4096 — reduced across ranks by the
+    native NCCL communicator (tg_comm_init_nccl)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1610_03525_b200 as pt
+    from paper_1610_03525_b200 import _abi
+    from paper_1610_03525_b200.shard import Comm, DeviceBackend, plan_band, terrain_stats
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=T5, base_frequency=F05,
+                       octaves=OCT5)
+    ccfg = cfg.to_c()
+    sizes, lags = [2, 4, 8, 16, 32, 64], [1 << i for i in range(13)]
+    band = plan_band(T5, T5, world, rank, align=1024, max_lag=max(lags))
+    out = torch.empty((band.rows, T5), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    def gen():
+        assert lib.tg_fbm_generate_rect_f32(C.byref(ccfg), 0, band.y0, T5, band.rows, out.data_ptr(), T5,
+                                            stream) == 0, _abi.last_error()
+
+    gen()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        gen()
+    e1.record()
+    torch.cuda.synchronize()
+    g = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(g, op=torch.distributed.ReduceOp.MAX)
+    gen_ms = float(g.item())
+    del out
+    res = {"workload": f"config 5: {T5}^2 zg_paper S5, {OCT5} octaves, base cell 1024 px, {world} row band(s)",
+           "gen_ms": gen_ms, "sample_octaves_per_s": float(T5) * T5 * OCT5 / (gen_ms * 1e-3),
+           "band_rows": band.rows, "scaling": "strong (fixed 32768^2 terrain)"}
+    if not analysis:
+        return res
+    comm = Comm.nccl(device=dev)
+    be = DeviceBackend(cfg, device=dev)
+    terrain_stats(band, be, comm, sizes, lags)  # warm-up (module loading, band buffer)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    st = terrain_stats(band, be, comm, sizes, lags)
+    torch.cuda.synchronize()
+    a = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
+    comm.close()
+    res.update({"analysis_ms": float(a.item()) * 1e3,
+                "analysis_note": "tg_terrain_stats_band per rank (band + halo/lookahead regenerated, median, "
+                                 "coastline + box count, variogram 13 lags x 2 axes), statistics all-reduced "
+                                 "by NCCL; host wall clock, max over ranks",
+                "sea_level": st.sea_level, "land_fraction": st.land_fraction, "box_counts": st.counts,
+                "d_box": st.d_box, "hurst": st.hurst, "d_variogram": st.d_variogram})
+    return res
 
 
 class ClockSampler:
@@ -306,6 +380,106 @@ def run_reference_arm(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_cfg5_workload(args, rank: int, world: int, local: int) -> None:
+    """--workload cfg5: the headline is config 5's generation — the 32768^2
+    terrain (f0 = 32, 16 octaves, zg_paper S5) in N row bands, one per rank,
+    K back-to-back band launches (CUDA events, max over ranks); value = the
+    whole terrain's sample-octaves per second (strong scaling).  e2e: each
+    rank's band through the drop-in generate_into(span<double>) as 4096^2
+    chunks into pinned host memory.  Then the NCCL-reduced statistics."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1610_03525_b200 as pt
+    from paper_1610_03525_b200 import _abi
+    from paper_1610_03525_b200.shard import plan_band
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _abi.load()
+    cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=T5, base_frequency=F05,
+                       octaves=OCT5)
+    ccfg = cfg.to_c()
+    band = plan_band(T5, T5, world, rank, align=1024, max_lag=4096)
+    peak_tflops = pt.ffma_peak_tflops()
+    out = [torch.empty((band.rows, T5), dtype=torch.float32, device="cuda") for _ in range(2)]
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+
+    def launch(i):
+        if lib.tg_fbm_generate_rect_f32(C.byref(ccfg), 0, band.y0, T5, band.rows, out[i % 2].data_ptr(), T5, sp):
+            raise RuntimeError(_abi.last_error())
+
+    with torch.cuda.stream(stream):
+        for i in range(max(args.warmup, 3)):
+            launch(i)
+    torch.cuda.synchronize()
+    K = max(1, min(args.steps, 20))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for i in range(K):
+                launch(i)
+            ev[1].record(stream)
+        torch.cuda.synchronize()
+    t = torch.tensor([ev[0].elapsed_time(ev[1])], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    so_step = float(T5) * T5 * OCT5
+    value = so_step * K / (total_ms * 1e-3)
+    per_rank_s = total_ms * 1e-3 / K
+    achieved = FLOPS_PER_SAMPLE_OCTAVE * band.rows * T5 * OCT5 / per_rank_s / 1e12
+    del out
+    torch.cuda.empty_cache()
+    # e2e: the drop-in over the rank's band in 4096^2 chunks, pinned host doubles
+    C4 = 4096
+    host = torch.empty((C4, C4), dtype=torch.float64, pin_memory=True)
+    chunks = [(x, y) for y in range(band.y0, band.y0 + band.rows, C4) for x in range(0, T5, C4)]
+    for (x, y) in chunks[:2]:
+        assert lib.tg_fbm_generate_f64_host(C.byref(ccfg), x, y, C4, host.data_ptr(), C4 * C4) == 0, _abi.last_error()
+    if world > 1:
+        dist.barrier()
+    e2e_steps = 2
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for (x, y) in chunks:
+            assert lib.tg_fbm_generate_f64_host(C.byref(ccfg), x, y, C4, host.data_ptr(), C4 * C4) == 0
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = so_step * e2e_steps / float(te.item())
+    stats = cfg5_terrain(lib, world, rank, steps=1, analysis=not args.no_analysis)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": max(args.warmup, 3), "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config 5: {T5}x{T5} fp32 fBm, zg_paper C2 (S5), {OCT5} octaves, base cell "
+                                   f"1024 px (f0 = 32), row bands over {world} GPU(s)",
+                       "parallelism": f"{world} row bands (no data-path collective; statistics NCCL-reduced)",
+                       "l2": f"2 rotating {band.rows * T5 * 4 >> 20} MiB band outputs (> 126 MB L2)"},
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tflops, "traffic": None,
+                         "note": f"{FLOPS_PER_SAMPLE_OCTAVE} flop/sample-octave x the slowest rank's band"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(ccfg) * len(chunks),
+                    "d2h_bytes_per_step": band.rows * T5 * 8, "steps": e2e_steps,
+                    "note": "tg_fbm_generate_f64_host (drop-in generate_into span<double>) per 4096^2 chunk of "
+                            "each rank's band into pinned host memory; max over ranks"},
+            "gpu_launches": K, "clocks": clk.summary(), "cpu_baseline": None,
+            "cfg5_terrain": stats,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -315,6 +489,10 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-analysis", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
+                    help="cfg2 (default): config 2 per rank (weak scaling); cfg5: the 32768^2 config-5 terrain "
+                         "in N row bands (strong scaling) with NCCL-reduced statistics")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 terrain section of the cfg2 line")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -323,6 +501,9 @@ def main() -> None:
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+        return
+    if args.workload == "cfg5":
+        run_cfg5_workload(args, rank, world, local)
         return
 
     import torch
@@ -437,6 +618,14 @@ def main() -> None:
             analysis = analysis_pass(lib, ccfg, bufs[(K - 1) % 3], sp, world, rank)
         except Exception as e:  # pragma: no cover
             analysis = {"error": str(e)}
+    terrain5 = None
+    if not args.no_cfg5:
+        del bufs
+        torch.cuda.empty_cache()
+        try:
+            terrain5 = cfg5_terrain(lib, world, rank, steps=3, analysis=not args.no_analysis)
+        except Exception as e:  # pragma: no cover
+            terrain5 = {"error": str(e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -489,13 +678,16 @@ def main() -> None:
                     "d2h_gbs": R * R * 8 / statistics.median(e2e_each) / 1e9,
                     "pageable_ms_per_step_median": statistics.median(pg_each) * 1e3,
                     "note": "tg_fbm_generate_f64_host (drop-in generate_into span<double>) into pinned host "
-                            "memory; input is the config struct only; the 128 MiB of doubles cross PCIe "
-                            "(device-widened bands, ~53 GB/s); pageable_ms: the same call into a pageable "
-                            "buffer (fp32 bands over PCIe, widened by the host pool)"},
+                            "memory; input is the config struct only; fp32 bands cross PCIe (64 MiB) and "
+                            "are widened to the caller's doubles by the host pool while later bands are in "
+                            "flight (a measured fraction of bands is widened on the device instead when the "
+                            "host is slower, capi.cu generate_host); pageable_ms: the same call into a "
+                            "pageable buffer"},
             "gpu_launches": K,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "analysis": analysis,
+            "cfg5_terrain": terrain5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

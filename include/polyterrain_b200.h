@@ -263,6 +263,89 @@ int tg_histogram_f32(const float* dev_rows, int64_t width, int64_t rows, int64_t
                      uint32_t prefix, uint32_t mask, int32_t shift, int32_t bits,
                      uint64_t* out_hist, void* stream);
 
+/* ---- multi-GPU terrain ----------------------------------------- */
+/* A large terrain splits into contiguous row bands, one per rank (one process
+ * per GPU), generated with no exchange at all (every sample is a function of
+ * (config, global pixel), fbm.hpp:7-8); the analysis regenerates a 1-row halo
+ * and max_lag lookahead rows locally, and only statistics cross GPUs.
+ * Replaces, for a sharded caller, fbm::generate_region (fbm.hpp:658-685) per
+ * band + analysis::coastline_mask / box_count (analysis.hpp:213-305) on the
+ * whole map; the reference's analogue of ranks are its row-band threads
+ * (fbm.hpp:609-622). */
+
+/* Communicator for the statistics all-reduces.  NCCL (over NVLink/NVSwitch on
+ * a B200 node): rank 0 calls tg_comm_unique_id and hands the 128 bytes to
+ * every rank over any host channel; libnccl.so.2 is loaded at run time.  Host
+ * hook: the caller's own transport (MPI, TCP, torch.distributed/gloo) reduces
+ * host buffers in place. */
+typedef struct tg_comm tg_comm;
+typedef int (*tg_allreduce_fn)(void* ctx, void* host_buf, uint64_t count,
+                               int32_t dtype /* 0 int64, 1 float64 */,
+                               int32_t op /* 0 sum, 1 max */);
+int tg_comm_unique_id(uint8_t id_out[128]);
+int tg_comm_init_nccl(const uint8_t id[128], int32_t nranks, int32_t rank, tg_comm** out);
+int tg_comm_init_host(tg_allreduce_fn fn, void* ctx, int32_t nranks, int32_t rank, tg_comm** out);
+int tg_comm_allreduce(tg_comm* comm, void* host_buf, uint64_t count, int32_t dtype, int32_t op);
+int tg_comm_destroy(tg_comm* comm);
+
+/* The terrain window and one rank's band of it (rows are global). */
+typedef struct {
+    int64_t x0, width;      /* columns */
+    int64_t y_origin, height;  /* rows [y_origin, y_origin + height) */
+    int32_t align;          /* band starts are multiples of align (box sizes, octave-0 cells) */
+    int32_t max_lag;        /* largest vertical variogram lag: lookahead rows below a band */
+} tg_terrain;
+typedef struct {
+    int64_t y0, rows;       /* owned rows [y0, y0 + rows), global */
+    int64_t halo_top;       /* regenerated rows above (0 or 1) */
+    int64_t below;          /* regenerated rows below: max(1, max_lag) clipped to the terrain */
+} tg_band;
+/* Host only: `world` contiguous bands whose starts are multiples of align,
+ * sizes differing by at most align rows. */
+int tg_plan_band(const tg_terrain* t, int32_t world, int32_t rank, tg_band* out);
+
+#define TG_MAX_BOX_SIZES 16
+#define TG_MAX_LAGS 32
+typedef struct {
+    double sea_level;       /* upper median of the whole terrain (analysis.hpp:244-250) or given */
+    double land_fraction;
+    int64_t land_pixels, coast_pixels;
+    int32_t n_sizes, n_lags;
+    int64_t counts[TG_MAX_BOX_SIZES];  /* box counts, whole terrain */
+    double d_box, k_box, r2_box;       /* D = -slope of log N vs log eps (analysis.hpp:299-305) */
+    double sum_sq[TG_MAX_LAGS][2];     /* variogram sums per lag, axis (0 x, 1 y) */
+    int64_t pairs[TG_MAX_LAGS][2];
+    double gamma[TG_MAX_LAGS];         /* both axes pooled: sum / (2 pairs) */
+    double hurst, d_variogram;         /* slope / 2 of log gamma vs log h; D = 3 - H */
+} tg_terrain_stats;
+
+/* Product path: generate this rank's band (+ halo / lookahead) on the
+ * current device, then the distributed statistics (sea level by a 3-pass
+ * radix select over all-reduced histograms unless *sea_level is given).
+ * Collective: every rank calls it with the same terrain, sizes and lags. */
+int tg_terrain_stats_band(const tg_fbm_config* cfg, const tg_terrain* t, const tg_band* band,
+                          const int32_t* sizes, int32_t n_sizes, const int32_t* lags,
+                          int32_t n_lags, const double* sea_level, tg_comm* comm,
+                          tg_terrain_stats* out, void* stream);
+
+/* The same driver over caller-supplied band operations — the test hook of the
+ * host logic (the reference's Source policy plays this role for generation,
+ * fbm.hpp:110-133).  The product path above never uses it. */
+typedef struct {
+    void* ctx;
+    int (*generate)(void* ctx, const tg_band* band);
+    int (*histogram)(void* ctx, uint32_t prefix, uint32_t mask, int32_t shift, int32_t bits,
+                     uint64_t* out_hist);
+    int (*boxcount)(void* ctx, double sea_level, const int32_t* sizes, int32_t n_sizes,
+                    int64_t* out_counts, int64_t* out_coast, int64_t* out_land);
+    int (*variogram)(void* ctx, const int32_t* lags, int32_t n_lags, double* out_sum_sq,
+                     int64_t* out_pairs);
+} tg_band_ops;
+int tg_terrain_stats_ops(const tg_terrain* t, const tg_band* band, const int32_t* sizes,
+                         int32_t n_sizes, const int32_t* lags, int32_t n_lags,
+                         const double* sea_level, tg_comm* comm, const tg_band_ops* ops,
+                         tg_terrain_stats* out);
+
 /* ---- measurement helpers ---------------------------------------------------- */
 
 /* FP32 FFMA-chain peak on the current device (TFLOP/s), for the roofline

@@ -21,6 +21,7 @@ TG_METHOD_GENERIC = 2
 TG_METHOD_PERLIN3 = 3
 TG_METHOD_PERLIN5 = 4
 TG_METHOD_OPENSIMPLEX = 5
+TG_METHOD_PERLIN_PERM = 6
 
 TG_MAX_RESOLUTION = 1 << 22
 TG_MAX_EXTENT = 1 << 17
@@ -31,6 +32,10 @@ TG_LANE_ANGLE = 0xA0761D6478BD642F
 TG_LANE_MAGNITUDE = 0xE7037ED1A0B428DB
 TG_LANE_SIMPLEX = 0x8EBC6AF09C88C6E3
 TG_PACK_K5 = 0xA24BAED4963EE407
+TG_LANE_PERM = 0x5851F42D4C957F2D
+TG_PERM_KI = 0xD1B54A32D192ED03
+TG_MAX_BOX_SIZES = 16
+TG_MAX_LAGS = 32
 
 
 class TgFbmConfig(C.Structure):
@@ -83,6 +88,40 @@ P = C.c_void_p
 PCFG = C.POINTER(TgFbmConfig)
 I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 
+class TgTerrain(C.Structure):
+    """tg_terrain: the terrain window of a sharded run."""
+
+    _fields_ = [("x0", C.c_int64), ("width", C.c_int64), ("y_origin", C.c_int64), ("height", C.c_int64),
+                ("align", C.c_int32), ("max_lag", C.c_int32)]
+
+
+class TgBand(C.Structure):
+    """tg_band: one rank's rows (global) plus regenerated halo / lookahead."""
+
+    _fields_ = [("y0", C.c_int64), ("rows", C.c_int64), ("halo_top", C.c_int64), ("below", C.c_int64)]
+
+
+class TgTerrainStats(C.Structure):
+    _fields_ = [("sea_level", C.c_double), ("land_fraction", C.c_double), ("land_pixels", C.c_int64),
+                ("coast_pixels", C.c_int64), ("n_sizes", C.c_int32), ("n_lags", C.c_int32),
+                ("counts", C.c_int64 * 16), ("d_box", C.c_double), ("k_box", C.c_double), ("r2_box", C.c_double),
+                ("sum_sq", (C.c_double * 2) * 32), ("pairs", (C.c_int64 * 2) * 32), ("gamma", C.c_double * 32),
+                ("hurst", C.c_double), ("d_variogram", C.c_double)]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_int32)
+OPS_GENERATE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(TgBand))
+OPS_HISTOGRAM = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int32, C.c_int32, C.c_void_p)
+OPS_BOXCOUNT = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                           C.c_void_p)
+OPS_VARIOGRAM = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p)
+
+
+class TgBandOps(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("generate", OPS_GENERATE), ("histogram", OPS_HISTOGRAM),
+                ("boxcount", OPS_BOXCOUNT), ("variogram", OPS_VARIOGRAM)]
+
+
 # name -> (restype, argtypes); every symbol include/polyterrain_b200.h declares.
 SIGNATURES = {
     "tg_abi_version": (C.c_int, []),
@@ -115,6 +154,16 @@ SIGNATURES = {
     "tg_histogram_f32": (C.c_int, [P, I64, I64, I64, C.c_uint32, C.c_uint32, I32, I32, P, P]),
     "tg_variogram_f32": (C.c_int, [P, I64, I64, I64, P, I32, P, P, P]),
     "tg_measure_ffma_peak": (C.c_int, [C.POINTER(F64), C.POINTER(F64)]),
+    "tg_comm_unique_id": (C.c_int, [P]),
+    "tg_comm_init_nccl": (C.c_int, [P, I32, I32, C.POINTER(C.c_void_p)]),
+    "tg_comm_init_host": (C.c_int, [ALLREDUCE_FN, P, I32, I32, C.POINTER(C.c_void_p)]),
+    "tg_comm_allreduce": (C.c_int, [P, P, U64, I32, I32]),
+    "tg_comm_destroy": (C.c_int, [P]),
+    "tg_plan_band": (C.c_int, [C.POINTER(TgTerrain), I32, I32, C.POINTER(TgBand)]),
+    "tg_terrain_stats_band": (C.c_int, [PCFG, C.POINTER(TgTerrain), C.POINTER(TgBand), P, I32, P, I32,
+                                        C.POINTER(F64), P, C.POINTER(TgTerrainStats), P]),
+    "tg_terrain_stats_ops": (C.c_int, [C.POINTER(TgTerrain), C.POINTER(TgBand), P, I32, P, I32, C.POINTER(F64), P,
+                                       C.POINTER(TgBandOps), C.POINTER(TgTerrainStats)]),
 }
 
 _lib = None

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libpolyterrain_b200.so")
 SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "perm2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu",
-           "hostpipe.cpp"]
+           "hostpipe.cpp", "terrain.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         objs.append(obj)
     os.makedirs(os.path.dirname(target), exist_ok=True)
     tmp = target + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread", "-ldl"]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"link failed:\n{out.stderr}")

@@ -46,7 +46,7 @@ class OracleBackend:
         if b.halo_top:
             up[0] = land[r0 - 1]
         dn[:-1] = own[1:]
-        if b.y0 + b.rows < b.height:
+        if not b.is_last:
             dn[-1] = land[r0 + b.rows]
         lf = np.ones_like(own)
         rt = np.ones_like(own)

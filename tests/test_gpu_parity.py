@@ -609,3 +609,25 @@ def test_perm_perlin_region_batch_and_zero():
         pt.generate_into_device(pt.FbmConfig(method=pt.Method.perlin_perm, seed=s, resolution=256,
                                              base_frequency=4, octaves=5), (0, 0), 256, one)
         assert torch.equal(out[i], one)
+
+
+def test_native_nccl_comm_one_rank_and_terrain_stats(oracle):
+    # tg_comm_init_nccl with one rank (no torch.distributed): the NCCL
+    # all-reduce path runs for real; the statistics equal the host-comm ones
+    from paper_1610_03525_b200.shard import Comm, DeviceBackend, plan_band, terrain_stats
+
+    comm = Comm.nccl(device=torch.device("cuda", 0))
+    a = comm.allreduce(np.array([1, 2, 3], dtype=np.int64))
+    assert list(a) == [1, 2, 3]
+    f = comm.allreduce(np.array([0.5, -2.0]), op="max")
+    assert list(f) == [0.5, -2.0]
+    cfgp = pt.FbmConfig(method=0, smoothstep=5, seed=3, resolution=1024, base_frequency=4, octaves=12)
+    sizes, lags = [2, 4, 8, 16, 32, 64], [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
+    band = plan_band(1024, 1024, 1, 0, align=256, max_lag=512)
+    s1 = terrain_stats(band, DeviceBackend(cfgp), comm, sizes, lags)
+    s2 = terrain_stats(band, DeviceBackend(cfgp), Comm(), sizes, lags)
+    comm.close()
+    assert s1.sea_level == s2.sea_level and s1.counts == s2.counts and s1.coast_pixels == s2.coast_pixels
+    # (the variogram sums use fp64 atomics across CTAs: equal to rounding, not bit for bit)
+    assert np.array_equal(s1.pairs, s2.pairs) and np.allclose(s1.sum_sq, s2.sum_sq, rtol=1e-12, atol=0)
+    assert 1.0 < s1.d_box < 2.0 and 2.0 < s1.d_variogram < 3.0

@@ -1,29 +1,73 @@
-"""Config 5: a 32768^2 terrain, 16 octaves, zg_paper S5, base cell 1024 px
-(f0 = 32), generated as row bands (one per rank) followed by the fractal
-analysis (median sea level, coastline + box count eps 2..64, variogram over
-lags 1..4096), statistics all-reduced across ranks.
+"""Config 5: the 32768^2 terrain, 16 octaves, zg_paper S5, base cell 1024 px
+(f0 = 32), as row bands (one per rank) followed by the fractal statistics of
+the whole terrain (median sea level, coastline + box count eps 2..64,
+variogram over lags 1..4096) through the C-ABI driver tg_terrain_stats_band,
+reduced across ranks by the native NCCL communicator.
 
     python tools/terrain_run.py                      # 1 GPU
     torchrun --nproc-per-node 8 --master-addr 127.0.0.1 tools/terrain_run.py
 
-Prints one JSON line (rank 0): generation time (max over ranks), sample-
-octaves/s, analysis time, box-count and variogram dimensions.
+Prints one JSON line (rank 0): bench.cfg5_terrain's numbers plus a per-phase
+breakdown of the analysis on rank 0 (the same C-ABI calls the driver makes,
+timed one by one with syncs).
 """
+import ctypes as C
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import bench  # noqa: E402
 import paper_1610_03525_b200 as pt  # noqa: E402
-from paper_1610_03525_b200.shard import Comm, DeviceBackend, plan_band, terrain_stats  # noqa: E402
+from paper_1610_03525_b200 import _abi  # noqa: E402
+from paper_1610_03525_b200.shard import plan_band  # noqa: E402
 
-T = int(os.environ.get("TG_T", "32768"))
-OCT = 16
+
+def phases(lib, world, rank):
+    """Rank 0's band: generation of band + halo + lookahead, the three median
+    histogram passes, coastline + box count, variogram — each synchronised."""
+    T = bench.T5
+    cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=T, base_frequency=bench.F05,
+                       octaves=bench.OCT5)
+    c = cfg.to_c()
+    band = plan_band(T, T, world, rank, align=1024, max_lag=4096)
+    buf = torch.empty((band.gen_rows, T), dtype=torch.float32, device="cuda")
+    own = buf.data_ptr() + 4 * band.halo_top * T
+    out = {}
+
+    def t(name, fn, reps=2):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        out[name] = round((time.perf_counter() - t0) / reps * 1e3, 3)
+
+    t("regenerate_band_ms", lambda: lib.tg_fbm_generate_rect_f32(C.byref(c), 0, band.gen_y0, T, band.gen_rows,
+                                                                 buf.data_ptr(), T, None))
+    hist = np.zeros(2048, dtype=np.uint64)
+    t("median_histograms_ms", lambda: [lib.tg_histogram_f32(own, T, band.rows, T, 0, 0, sh, bits, hist.ctypes.data,
+                                                            None) for sh, bits in ((21, 11), (10, 11), (0, 10))])
+    sz = (C.c_int32 * 6)(2, 4, 8, 16, 32, 64)
+    cnt = (C.c_int64 * 6)()
+    a, b = C.c_int64(), C.c_int64()
+    t("coastline_boxcount_ms", lambda: lib.tg_coastline_boxcount_band(own, T, band.rows, T, band.halo_top,
+                                                                      0 if band.is_last else 1, 0.0, sz, 6, cnt,
+                                                                      C.byref(a), C.byref(b), None))
+    lg = (C.c_int32 * 13)(*[1 << i for i in range(13)])
+    ss = (C.c_double * 26)()
+    pr = (C.c_int64 * 26)()
+    t("variogram_ms", lambda: lib.tg_variogram_band_f32(own, T, band.rows + band.below, T, band.rows, lg, 13, ss,
+                                                        pr, None))
+    return out
 
 
 def main():
@@ -33,69 +77,15 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=T, base_frequency=T // 1024,
-                       octaves=OCT)
-    sizes = [2, 4, 8, 16, 32, 64]
-    lags = [1 << i for i in range(13)]
-    band = plan_band(T, T, world, rank, align=1024, max_lag=max(lags))
-    be = DeviceBackend(cfg)
-    comm = Comm(device=torch.device("cuda", local))
-    # warm-up generation of the band (allocations, LUTs)
-    be.generate(band)
-    torch.cuda.synchronize()
-    # timed generation of the owned rows only (the throughput number)
-    out = torch.empty((band.rows, T), dtype=torch.float32, device="cuda")
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    pt.generate_rect_device(cfg, (0, band.y0), T, band.rows, out)
-    e1.record()
-    torch.cuda.synchronize()
-    gen_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(gen_ms, op=dist.ReduceOp.MAX)
-    del out
-    # analysis: regenerates the band + halo/lookahead rows, all-reduces
-    # statistics; one untimed warm-up pass (module loading, pool growth)
-    terrain_stats(band, be, comm, sizes, lags)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    phases = {}
-
-    def timed(name, fn):
-        def w(*a, **k):
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            r = fn(*a, **k)
-            torch.cuda.synchronize()
-            phases[name] = phases.get(name, 0.0) + (time.perf_counter() - t) * 1e3
-            return r
-        return w
-
-    be.generate = timed("regenerate_band_ms", be.generate)
-    be.histogram = timed("median_histograms_ms", be.histogram)
-    be.boxcount = timed("coastline_boxcount_ms", be.boxcount)
-    be.variogram = timed("variogram_ms", be.variogram)
-    t0 = time.perf_counter()
-    st = terrain_stats(band, be, comm, sizes, lags)
-    torch.cuda.synchronize()
-    an_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(an_s, op=dist.ReduceOp.MAX)
+    lib = _abi.load()
+    res = bench.cfg5_terrain(lib, world, rank, steps=3, analysis=True)
+    torch.cuda.empty_cache()
+    ph = phases(lib, world, rank) if rank == 0 else None
     if rank == 0:
-        so = T * T * OCT
-        print(json.dumps({
-            "workload": f"config 5: {T}^2 zg_paper S5, {OCT} octaves, base cell 1024 px, {world} row bands",
-            "n_gpus": world, "gen_ms": float(gen_ms.item()), "sample_octaves_per_s": so / (gen_ms.item() * 1e-3),
-            "analysis_s": float(an_s.item()), "analysis_phases_ms_rank0": {k: round(v, 3) for k, v in phases.items()},
-            "sea_level": st.sea_level, "land_fraction": st.land_fraction,
-            "box_counts": st.counts, "d_box": st.d_box, "r2_box": st.r2_box,
-            "variogram_gamma": [float(g) for g in st.gamma], "hurst": st.hurst, "d_variogram": st.d_variogram,
-        }), flush=True)
+        res["analysis_phases_ms_rank0"] = ph
+        print(json.dumps(res), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
