@@ -324,7 +324,7 @@ def traffic_from_profiles():
         return None
 
 
-def cpu_reference_run(steps: int, warmup: int, target_s: float | None = None):
+def cpu_reference_run(steps: int, warmup: int, target_s: float | None = None, threads: int | None = None):
     """The unmodified reference (oracle/_ref/libtgref.so, bench::run_bench
     protocol, bench.hpp:54-78) on this host's cores.  zg with the quintic fade
     is not expressible in the reference FbmConfig: timed as the
@@ -334,7 +334,7 @@ def cpu_reference_run(steps: int, warmup: int, target_s: float | None = None):
     from paper_1610_03525_b200._abi import TgFbmConfig
 
     ref = Reference()
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     c = TgFbmConfig()
     c.seed, c.method, c.smoothstep, c.octaves, c.threads = 1, 0, 0, OCTAVES, cores
     c.resolution, c.base_frequency, c.frequency_ratio, c.persistence, c.base_amplitude = R, F0, 2.0, 0.5, 1.0
@@ -638,6 +638,13 @@ def main() -> None:
                               f"{r['cpu']}")}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+        try:  # bench.hpp:54-78 is also quoted single-threaded (the CLI forces threads = 1, terrain_cli.cpp:403)
+            r1 = cpu_reference_run(0, 0, target_s=10.0, threads=1)
+            cpu["threads_1"] = {"value": r1["value"], "cores": 1,
+                                "sample": f"{r1['reps']} full {R}^2 x {OCTAVES}-octave maps, threads=1, median "
+                                          f"{r1['median_s']*1e3:.1f} ms"}
+        except Exception as e:  # pragma: no cover
+            cpu["threads_1"] = {"value": None, "sample": f"failed: {e}"}
 
     if rank == 0:
         line = {

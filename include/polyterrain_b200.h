@@ -149,6 +149,20 @@ int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_
  * the global pixel).  Unlike the square form (fbm.hpp:551-558) the origin
  * need not sit on an octave-0 cell boundary, so shards can regenerate halo
  * rows; |origin| <= 2^40 still applies. */
+/* generate_region / generate_heightmap with cfg->normalize (fbm.hpp:638-685):
+ * the extent^2 map normalised to [-1, 1] on the device in fp64 (min / max of
+ * the samples, -1 + 2 (v - lo) / (hi - lo), fbm.hpp:653) and written to the
+ * host doubles; a constant map is returned unchanged with *constant_source = 1.
+ * out_min / out_max: the source range.  Synchronous. */
+int tg_fbm_generate_normalized_f64_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy,
+                                        int32_t extent, double* host_out, uint64_t n_out,
+                                        double* out_min, double* out_max, int32_t* constant_source);
+/* Per-octave device seconds of a generation over the window (the drop-in's
+ * octave_seconds, fbm.hpp:564,624-626): the increments T(k+1) - T(k) of
+ * diagnostic launches of the octave prefixes (the fused kernel renders all
+ * octaves in one pass).  seconds_out: cfg->octaves entries.  Synchronous. */
+int tg_fbm_octave_times(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int32_t extent,
+                        double* seconds_out, void* stream);
 int tg_fbm_generate_rect_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t width,
                              int64_t height, float* dev_out, int64_t ld, void* stream);
 /* A batch of maps that differ only in seed: out[b] is the window for

@@ -14,8 +14,10 @@
 //     quintic zero-gradient kernel is expressible, and
 //     `zero_lattice` replaces the ZeroSource template policy.
 //   * resolution/extent caps are lifted to 2^22 / 2^17.
-//   * octave_seconds has one entry per octave (the fused kernel cannot time
-//     octaves separately; the call's wall time is split evenly).
+//   * octave_seconds has one entry per octave: octave k's device time as the
+//     increment between diagnostic launches of the octave prefixes 0..k
+//     (tg_fbm_octave_times; the fused kernel renders every octave in one
+//     pass, so they are measured when requested, at extra cost).
 //   * `threads` is validated like the reference and otherwise ignored.
 
 #include <array>
@@ -189,8 +191,12 @@ inline void generate_into(const FbmConfig& cfg, std::array<long long, 2> origin,
         const auto w = detail::subpixel_warnings(cfg);
         warnings->insert(warnings->end(), w.begin(), w.end());
     }
-    if (octave_seconds)
-        for (int o = 0; o < cfg.octaves; ++o) octave_seconds->push_back(dt / cfg.octaves);
+    (void)dt;
+    if (octave_seconds) {
+        std::vector<double> t(static_cast<std::size_t>(cfg.octaves));
+        check(tg_fbm_octave_times(&c, origin[0], origin[1], extent, t.data(), nullptr));
+        octave_seconds->insert(octave_seconds->end(), t.begin(), t.end());
+    }
 }
 
 // normalize_map (fbm.hpp:638-656)
@@ -224,8 +230,21 @@ inline Heightmap generate_region(const FbmConfig& cfg, std::array<long long, 2> 
     if (extent < 1 || extent > TG_MAX_EXTENT)
         throw ValidationError("generate: extent must be in [1, 131072]");
     hm.data.resize(static_cast<std::size_t>(extent) * static_cast<std::size_t>(extent));
-    generate_into(cfg, origin, extent, hm.data, &hm.octave_seconds, &hm.warnings);
-    if (cfg.normalize) return normalize_map(hm);
+    if (!cfg.normalize) {
+        generate_into(cfg, origin, extent, hm.data, &hm.octave_seconds, &hm.warnings);
+        return hm;
+    }
+    // normalize_map fused on the device (the same doubles as the host form)
+    const tg_fbm_config c = cfg.to_c();
+    std::int32_t constant = 0;
+    check(tg_fbm_generate_normalized_f64_host(&c, origin[0], origin[1], extent, hm.data.data(), hm.data.size(),
+                                              &hm.source_min, &hm.source_max, &constant));
+    hm.constant_source = constant != 0;
+    hm.normalized = constant == 0;
+    hm.octave_seconds.resize(static_cast<std::size_t>(cfg.octaves));
+    check(tg_fbm_octave_times(&c, origin[0], origin[1], extent, hm.octave_seconds.data(), nullptr));
+    const auto w = detail::subpixel_warnings(cfg);
+    hm.warnings.insert(hm.warnings.end(), w.begin(), w.end());
     return hm;
 }
 

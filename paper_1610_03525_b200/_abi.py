@@ -132,6 +132,9 @@ SIGNATURES = {
     "tg_device_count": (C.c_int, []),
     "tg_fbm_generate_f32": (C.c_int, [PCFG, I64, I64, I64, P, U64, P]),
     "tg_fbm_generate_rect_f32": (C.c_int, [PCFG, I64, I64, I64, I64, P, I64, P]),
+    "tg_fbm_octave_times": (C.c_int, [PCFG, I64, I64, I32, P, P]),
+    "tg_fbm_generate_normalized_f64_host": (C.c_int, [PCFG, I64, I64, I32, P, U64, C.POINTER(F64), C.POINTER(F64),
+                                                      C.POINTER(I32)]),
     "tg_fbm_generate_batch_f32": (C.c_int, [PCFG, P, I32, I64, I64, I64, I64, P, P]),
     "tg_fbm_generate_f64_host": (C.c_int, [PCFG, I64, I64, I64, P, U64]),
     "tg_fbm_generate_f32_host": (C.c_int, [PCFG, I64, I64, I64, P, U64]),

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -33,6 +34,8 @@ void fbm3d_tile(int* tx, int* ty, int* tz);
 void fbm3d_plan(Fbm3Args* a, int zg_sep_only);
 cudaError_t lattice_launch(int what, const tg_lattice_key* keys, uint64_t n, uint64_t lane,
                            void* out, cudaStream_t st);
+cudaError_t widen_normalize_launch(const float* in, double* out, uint64_t n, double lo, double span, int norm,
+                                   cudaStream_t st);
 cudaError_t widen_launch(const float* in, double* out, uint64_t n, cudaStream_t st);
 const float4* row_lut(int order);
 }  // namespace tg
@@ -480,6 +483,118 @@ int tg_fbm_generate_f32(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_
         return fail(TG_EVALIDATION, "generate: output buffer size mismatch");  // fbm.hpp:549
     if (int st = validate_window(cfg, ox, oy, extent, extent)) return st;  // fbm.hpp:551-558
     return tg_fbm_generate_rect_f32(cfg, ox, oy, extent, extent, dev_out, extent, stream);
+}
+
+// generate_region / generate_heightmap with cfg.normalize (fbm.hpp:638-685)
+// on the device: the map generated in fp32, its min / max reduced on the
+// device (exact: the extremes of the fp32 samples are those of the widened
+// doubles), then widened and normalised in fp64 band by band on the way to
+// the host — the same doubles as normalize_map on the host-widened map.
+int tg_fbm_generate_normalized_f64_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int32_t extent,
+                                        double* host_out, uint64_t n_out, double* out_min, double* out_max,
+                                        int32_t* constant_source) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (!host_out || !out_min || !out_max || !constant_source) return fail(TG_EVALIDATION, "generate: null output");
+    if (extent < 1 || extent > TG_MAX_EXTENT) return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
+    const uint64_t n = static_cast<uint64_t>(extent) * static_cast<uint64_t>(extent);
+    if (n_out != n) return fail(TG_EVALIDATION, "generate: output buffer size mismatch");
+    if (int st = validate_window(cfg, ox, oy, extent, extent)) return st;
+    if (int st = device_ready()) return st;
+    cudaStream_t s = nullptr;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    float* map = nullptr;
+    double* band = nullptr;
+    const uint64_t rows = std::max<uint64_t>(1, (uint64_t(8) << 20) / static_cast<uint64_t>(extent));
+    int st = TG_OK;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&map), sizeof(float) * n, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&band), sizeof(double) * rows * extent, s);
+    if (e != cudaSuccess) st = cuda_fail(e, "normalized generate alloc");
+    if (st == TG_OK) st = tg_fbm_generate_f32(cfg, ox, oy, extent, map, n, s);
+    double lo = 0, hi = 0;
+    if (st == TG_OK) st = tg_minmax_f32(map, n, &lo, &hi, s);
+    const int norm = lo != hi;
+    for (uint64_t r0 = 0; st == TG_OK && r0 < static_cast<uint64_t>(extent); r0 += rows) {
+        const uint64_t m = std::min<uint64_t>(rows, extent - r0) * extent;
+        e = tg::widen_normalize_launch(map + r0 * extent, band, m, lo, hi - lo, norm, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(host_out + r0 * extent, band, sizeof(double) * m,
+                                                  cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "normalized generate");
+    }
+    if (map) cudaFreeAsync(map, s);
+    if (band) cudaFreeAsync(band, s);
+    e = cudaStreamSynchronize(s);
+    if (st == TG_OK && e != cudaSuccess) st = cuda_fail(e, "normalized generate sync");
+    cudaStreamDestroy(s);
+    if (st != TG_OK) return st;
+    *out_min = lo;
+    *out_max = hi;
+    *constant_source = norm ? 0 : 1;
+    return TG_OK;
+}
+
+// Per-octave device time (generate_into's octave_seconds, fbm.hpp:564,
+// 624-626): the fused kernel renders every octave in one pass, so octave k's
+// time is measured as the increment T(k+1) - T(k) between diagnostic launches
+// of the octave prefixes 0..k over the same window (CUDA events, median of 3
+// after a warm-up; clamped at 0).  Costs about 4 (N + 1) extra launches.
+int tg_fbm_octave_times(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int32_t extent, double* seconds_out,
+                        void* stream) {
+    if (int st = validate_cfg(cfg)) return st;
+    if (!seconds_out) return fail(TG_EVALIDATION, "octave_times: null output");
+    if (extent < 1 || extent > TG_MAX_EXTENT) return fail(TG_EVALIDATION, "generate: extent must be in [1, 131072]");
+    if (int st = validate_window(cfg, ox, oy, extent, extent)) return st;
+    if (int st = device_ready()) return st;
+    // The times depend on the configuration's shape, not on the seed or the
+    // (aligned) origin: measured once per shape and device, then reused.
+    static std::mutex mu;
+    static std::map<std::string, std::vector<double>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    char keyb[256];
+    snprintf(keyb, sizeof(keyb), "%d|%d|%d|%d|%lld|%d|%.17g|%.17g|%.17g|%d|%d", dev, cfg->method, cfg->smoothstep,
+             cfg->octaves, static_cast<long long>(cfg->resolution), cfg->base_frequency, cfg->frequency_ratio,
+             cfg->persistence, cfg->base_amplitude, cfg->zero_lattice, extent);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(keyb);
+        if (it != cache.end()) {
+            std::copy(it->second.begin(), it->second.end(), seconds_out);
+            return TG_OK;
+        }
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float* buf = nullptr;
+    TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(float) * extent * extent, s));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<double> prefix_ms(static_cast<size_t>(cfg->octaves) + 1, 0.0);
+    int st = TG_OK;
+    for (int k = 1; k <= cfg->octaves && st == TG_OK; ++k) {
+        tg_fbm_config c = *cfg;
+        c.octaves = k;  // octaves 0..k-1: the same specs (repeated multiplication from octave 0)
+        double ms[3];
+        for (int r = -1; r < 3 && st == TG_OK; ++r) {
+            cudaEventRecord(e0, s);
+            st = tg_fbm_generate_rect_f32(&c, ox, oy, extent, extent, buf, extent, s);
+            cudaEventRecord(e1, s);
+            if (st == TG_OK && cudaEventSynchronize(e1) != cudaSuccess) st = fail(TG_EDEVICE, "octave_times sync");
+            float f = 0.f;
+            cudaEventElapsedTime(&f, e0, e1);
+            if (r >= 0) ms[r] = f;
+        }
+        if (st == TG_OK) prefix_ms[k] = std::max(std::min(ms[0], ms[1]), std::min(std::max(ms[0], ms[1]), ms[2]));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(buf, s);
+    if (st != TG_OK) return st;
+    std::vector<double> t(static_cast<size_t>(cfg->octaves));
+    for (int k = 0; k < cfg->octaves; ++k) t[k] = std::max(0.0, prefix_ms[k + 1] - prefix_ms[k]) * 1e-3;
+    std::copy(t.begin(), t.end(), seconds_out);
+    std::lock_guard<std::mutex> lock(mu);
+    cache[keyb] = std::move(t);
+    return TG_OK;
 }
 
 // texture::render (texture.hpp:50-72): marble / wood fused into the fBm

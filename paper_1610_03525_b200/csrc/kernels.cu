@@ -99,6 +99,24 @@ __global__ void widen_kernel(const float* __restrict__ in, double* __restrict__ 
         out[i] = static_cast<double>(in[i]);
 }
 
+// normalize_map (fbm.hpp:638-656) fused into the fp32 -> fp64 widening of
+// the drop-in's host copy: -1 + 2 (v - lo) / span in fp64 on the exactly
+// widened sample, the reference's expression and operation order (653).
+__global__ void widen_normalize_kernel(const float* __restrict__ in, double* __restrict__ out, uint64_t n,
+                                       double lo, double span, int norm) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double v = static_cast<double>(in[i]);
+        out[i] = norm ? -1.0 + 2.0 * (v - lo) / span : v;
+    }
+}
+
+cudaError_t widen_normalize_launch(const float* in, double* out, uint64_t n, double lo, double span, int norm,
+                                   cudaStream_t st) {
+    widen_normalize_kernel<<<148 * 8, 256, 0, st>>>(in, out, n, lo, span, norm);
+    return cudaGetLastError();
+}
+
 cudaError_t widen_launch(const float* in, double* out, uint64_t n, cudaStream_t st) {
     widen_kernel<<<148 * 8, 256, 0, st>>>(in, out, n);
     return cudaGetLastError();

@@ -245,9 +245,13 @@ def generate_into(cfg: FbmConfig, origin, extent: int, out: np.ndarray,
     if warnings is not None:
         warnings.extend(_warnings(cfg))
     if octave_seconds is not None:
-        # One fused launch covers all octaves: the total is split evenly so the
-        # reference contract octave_seconds.size() == octaves holds.
-        octave_seconds.extend([dt / cfg.octaves] * cfg.octaves)
+        # The fused kernel renders every octave in one pass: octave k's time is
+        # the device-time increment between diagnostic launches of the octave
+        # prefixes 0..k (tg_fbm_octave_times), one entry per octave as the
+        # reference's contract requires (fbm.hpp:564,624-626).
+        t = (C.c_double * cfg.octaves)()
+        _check(lib.tg_fbm_octave_times(C.byref(cfg.to_c()), int(origin[0]), int(origin[1]), int(extent), t, None))
+        octave_seconds.extend(list(t))
 
 
 def normalize_map(hm: Heightmap) -> Heightmap:
@@ -274,9 +278,22 @@ def generate_region(cfg: FbmConfig, origin, extent: int) -> Heightmap:
     if extent < 1 or extent > _abi.TG_MAX_EXTENT:
         raise ValidationError("generate: extent must be in [1, 131072]")
     hm.data = np.empty((extent, extent), dtype=np.float64)
-    generate_into(cfg, origin, extent, hm.data, hm.octave_seconds, hm.warnings)
-    if cfg.normalize:
-        return normalize_map(hm)
+    if not cfg.normalize:
+        generate_into(cfg, origin, extent, hm.data, hm.octave_seconds, hm.warnings)
+        return hm
+    # normalize_map fused on the device (the same doubles as the host form)
+    lib = _abi.load()
+    c = cfg.to_c()
+    lo, hi, const = C.c_double(), C.c_double(), C.c_int32()
+    _check(lib.tg_fbm_generate_normalized_f64_host(C.byref(c), int(origin[0]), int(origin[1]), int(extent),
+                                                   hm.data.ctypes.data, hm.data.size, C.byref(lo), C.byref(hi),
+                                                   C.byref(const)))
+    hm.source_min, hm.source_max = lo.value, hi.value
+    hm.constant_source, hm.normalized = bool(const.value), not const.value
+    t = (C.c_double * cfg.octaves)()
+    _check(lib.tg_fbm_octave_times(C.byref(c), int(origin[0]), int(origin[1]), int(extent), t, None))
+    hm.octave_seconds.extend(list(t))
+    hm.warnings.extend(_warnings(cfg))
     return hm
 
 

@@ -631,3 +631,53 @@ def test_native_nccl_comm_one_rank_and_terrain_stats(oracle):
     # (the variogram sums use fp64 atomics across CTAs: equal to rounding, not bit for bit)
     assert np.array_equal(s1.pairs, s2.pairs) and np.allclose(s1.sum_sq, s2.sum_sq, rtol=1e-12, atol=0)
     assert 1.0 < s1.d_box < 2.0 and 2.0 < s1.d_variogram < 3.0
+
+
+def test_race_stress_back_to_back_and_concurrent_streams():
+    # compute-sanitizer is closed on this GPU pool (it left GPUs needing a
+    # reset), so the shared-memory staging (pairwise named barriers over the
+    # dead ppc-1 grid) and the programmatic-dependent-launch early start are
+    # stress-tested instead: 48 back-to-back config-2 launches into distinct
+    # buffers on one stream (grids overlap their neighbours' tails), then two
+    # streams racing the same map, must all be bit-identical to an isolated
+    # launch — a race shows up as a nondeterministic pixel.
+    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=4096, base_frequency=8, octaves=12)
+    ref = gen(c, 0, 0, 2048, 1024)
+    torch.cuda.synchronize()
+    lib = _abi.load()
+    outs = [torch.empty((1024, 2048), dtype=torch.float32, device="cuda") for _ in range(48)]
+    s = torch.cuda.current_stream().cuda_stream
+    for o in outs:
+        assert lib.tg_fbm_generate_rect_f32(C.byref(c), 0, 0, 2048, 1024, o.data_ptr(), 2048, s) == 0
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    more = [torch.empty((1024, 2048), dtype=torch.float32, device="cuda") for _ in range(16)]
+    for i, o in enumerate(more):
+        st = (s1 if i % 2 else s2).cuda_stream
+        assert lib.tg_fbm_generate_rect_f32(C.byref(c), 0, 0, 2048, 1024, o.data_ptr(), 2048, st) == 0
+    torch.cuda.synchronize()
+    for o in outs + more:
+        assert torch.equal(o, ref)
+
+
+def test_device_normalized_heightmap_equals_host_normalize(oracle):
+    # generate_region with normalize: widening + normalize_map fused on the
+    # device must give the host form's doubles bit for bit (fbm.hpp:638-656)
+    for m in (0, 3, 6):
+        cfg = pt.FbmConfig(method=m, seed=13, resolution=512, base_frequency=4, octaves=9, normalize=True)
+        hm = pt.generate_region(cfg, (0, 0), 512)
+        raw = pt.generate_region(pt.FbmConfig(method=m, seed=13, resolution=512, base_frequency=4, octaves=9),
+                                 (0, 0), 512)
+        ref = pt.normalize_map(raw)
+        assert hm.normalized and np.array_equal(hm.data, ref.data)
+        assert hm.source_min == ref.source_min and hm.source_max == ref.source_max
+        assert len(hm.octave_seconds) == 9 and min(hm.octave_seconds) >= 0.0
+    z = pt.generate_region(pt.FbmConfig(seed=1, resolution=64, octaves=3, normalize=True, zero_lattice=True),
+                           (0, 0), 64)
+    assert z.constant_source and not z.normalized and np.all(z.data == 0.0)
+
+
+def test_octave_times_are_prefix_increments():
+    c = make_cfg(method=0, smoothstep=5, seed=1, resolution=4096, base_frequency=8, octaves=12)
+    t = (C.c_double * 12)()
+    assert _abi.load().tg_fbm_octave_times(C.byref(c), 0, 0, 4096, t, None) == 0, _abi.last_error()
+    assert all(v >= 0.0 for v in t) and 5e-6 < sum(t) < 5e-3
