@@ -24,6 +24,7 @@ CONFIGS = {
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--rotate", type=int, default=1, help="output buffers written in rotation (3: the bench's)")
 a = ap.parse_args()
 if a.config == "cfg4":
     cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_separable, resolution=512, base_frequency=8, octaves=8)
@@ -33,8 +34,9 @@ if a.config == "cfg4":
 else:
     kw, ext = CONFIGS[a.config]
     cfg = pt.FbmConfig(**kw)
-    out = torch.empty((ext, ext), dtype=torch.float32, device="cuda")
-    for _ in range(a.iters):
-        pt.generate_into_device(cfg, (0, 0), ext, out)
+    outs = [torch.empty((ext, ext), dtype=torch.float32, device="cuda") for _ in range(a.rotate)]
+    for i in range(a.iters):
+        pt.generate_into_device(cfg, (0, 0), ext, outs[i % a.rotate])
+    out = outs[0]
 torch.cuda.synchronize()
 print("ok", a.config, float(out.abs().max()))
