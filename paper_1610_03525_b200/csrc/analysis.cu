@@ -145,83 +145,89 @@ __global__ void __launch_bounds__(kBins / 2) radix_pick(SelectState* st, unsigne
 }
 
 // ---- coastline bit mask -------------------------------------------------------
-// One warp per 1024-pixel row segment (32 words).  coast = land & !(all four
-// neighbours land), neighbours outside the map count as land (the reference
-// only tests in-bounds neighbours).
+// coast = land & !(all four neighbours land); neighbours outside the map
+// count as land (the reference only tests in-bounds neighbours,
+// analysis.hpp:228-229).  A warp owns a 1024-pixel column segment (lane i
+// holds word w0 + i as a ballot of 32 land tests) and walks a strip of
+// kCoastRows rows down the map carrying the land words of the row above and
+// the current row, so every sample is read once (plus one halo row per strip)
+// instead of three times.
 // Band form: `rows` rows of width R (row pitch ld) starting at h; the rows
 // just above/below exist (h - ld, h + rows*ld) when has_top / has_bot — halos
 // regenerated by the caller for row-band shards.
-__global__ void coast_bits_kernel(const float* __restrict__ h, int64_t R, int64_t rows, int64_t ld,
-                                  int has_top, int has_bot, float sea,
+constexpr int kCoastRows = 32;
+
+// Land word of lane's w = w0 + lane in `row` (x >= R: not land).
+__device__ __forceinline__ uint32_t land_word(const float* __restrict__ row, int64_t w0, int64_t R, float sea,
+                                              int lane) {
+    uint32_t L = 0;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {  // all 16 loads of a half in flight before the ballots
+            const int64_t x = (w0 + 16 * half + i) * 32 + lane;
+            v[i] = x < R ? row[x] : -INFINITY;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t b = __ballot_sync(0xffffffffu, v[i] >= sea);
+            if (lane == 16 * half + i) L = b;
+        }
+    }
+    return L;
+}
+
+__global__ void __launch_bounds__(256, 4)
+coast_bits_kernel(const float* __restrict__ h, int64_t R, int64_t rows, int64_t ld,
+                                  int has_top, int has_bot, float sea, int srows,
                                   uint32_t* __restrict__ bits, uint8_t* __restrict__ mask8,
                                   unsigned long long* __restrict__ counts /* land, coast */) {
     const int64_t words = (R + 31) / 32;
     const int64_t segs = (words + 31) / 32;
+    const int64_t strips = (rows + srows - 1) / srows;
     const int lane = threadIdx.x & 31;
     const int64_t warp_global = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long land = 0, coast = 0;
-    for (int64_t t = warp_global; t < rows * segs; t += nwarps) {
-        const int64_t y = t / segs;
-        const int64_t w0 = (t - y * segs) * 32;
-        const float* row = h + y * ld;
-        const float* up = (y > 0 || has_top) ? row - ld : nullptr;
-        const float* dn = (y + 1 < rows || has_bot) ? row + ld : nullptr;
-        // land bits of this row and the neighbours, one word per iteration;
-        // lane i ends up owning word w0 + i.
-        uint32_t Lc = 0, Lu = 0, Ld = 0;
-        // two halves of 16 words: all 48 loads of a half are issued before the
-        // ballots (latency-bound otherwise); words past the row end read
-        // nothing (x >= R)
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            float vc[16], vu[16], vd[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t x = (w0 + 16 * half + i) * 32 + lane;
-                const bool in = x < R;
-                vc[i] = in ? row[x] : -INFINITY;
-                vu[i] = in && up ? up[x] : INFINITY;
-                vd[i] = in && dn ? dn[x] : INFINITY;
-            }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const uint32_t bc = __ballot_sync(0xffffffffu, vc[i] >= sea);
-                const uint32_t bu = __ballot_sync(0xffffffffu, vu[i] >= sea);
-                const uint32_t bd = __ballot_sync(0xffffffffu, vd[i] >= sea);
-                if (lane == 16 * half + i) {
-                    Lc = bc;
-                    Lu = bu;
-                    Ld = bd;
+    for (int64_t t = warp_global; t < strips * segs; t += nwarps) {
+        const int64_t st = t / segs;
+        const int64_t w0 = (t - st * segs) * 32;
+        const int64_t y0 = st * srows, y1 = min(rows, y0 + srows);
+        const int64_t w = w0 + lane;
+        const int64_t valid = R - w * 32;  // bits beyond R count as land for the horizontal test
+        const uint32_t beyond = valid >= 32 ? 0u : ~((1u << (valid > 0 ? valid : 0)) - 1u);
+        uint32_t Lu = (y0 > 0 || has_top) ? land_word(h + (y0 - 1) * ld, w0, R, sea, lane) : 0xffffffffu;
+        uint32_t Lc = land_word(h + y0 * ld, w0, R, sea, lane);
+        for (int64_t y = y0; y < y1; ++y) {
+            const float* row = h + y * ld;
+            const uint32_t Ld = (y + 1 < rows || has_bot) ? land_word(row + ld, w0, R, sea, lane) : 0xffffffffu;
+            // horizontal neighbours: bit b-1 / b+1 incl. the adjacent words' edge bits
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, Lc, 1);
+            const uint32_t next = __shfl_down_sync(0xffffffffu, Lc, 1);
+            if (w < words) {
+                uint32_t prev_hi, next_lo;
+                if (lane == 0)
+                    prev_hi = w == 0 ? 1u : (row[w * 32 - 1] >= sea ? 1u : 0u);
+                else
+                    prev_hi = prev >> 31;
+                if (lane == 31 || w + 1 >= words)
+                    next_lo = (w + 1) * 32 >= R ? 1u : (row[(w + 1) * 32] >= sea ? 1u : 0u);
+                else
+                    next_lo = next & 1u;
+                const uint32_t Lr = (Lc >> 1) | (next_lo << 31) | (beyond >> 1);  // land at x+1
+                const uint32_t Ll = (Lc << 1) | prev_hi;                         // land at x-1
+                const uint32_t coast_bits = Lc & ~(Ll & Lr & Lu & Ld);
+                if (bits) bits[y * words + w] = coast_bits;
+                land += __popc(Lc);
+                coast += __popc(coast_bits);
+                if (mask8) {
+                    const int64_t nbit = valid >= 32 ? 32 : valid;
+                    for (int b = 0; b < nbit; ++b) mask8[y * R + w * 32 + b] = (coast_bits >> b) & 1u;
                 }
             }
-        }
-        const int64_t w = w0 + lane;
-        // horizontal neighbours: bit b-1 / b+1 incl. the adjacent words' edge bits
-        const uint32_t prev = __shfl_up_sync(0xffffffffu, Lc, 1);
-        const uint32_t next = __shfl_down_sync(0xffffffffu, Lc, 1);
-        if (w < words) {
-            uint32_t prev_hi, next_lo;
-            if (lane == 0)
-                prev_hi = w == 0 ? 1u : (row[w * 32 - 1] >= sea ? 1u : 0u);
-            else
-                prev_hi = prev >> 31;
-            if (lane == 31 || w + 1 >= words)
-                next_lo = (w + 1) * 32 >= R ? 1u : (row[(w + 1) * 32] >= sea ? 1u : 0u);
-            else
-                next_lo = next & 1u;
-            const int64_t valid = R - w * 32;  // bits beyond R count as land
-            const uint32_t beyond = valid >= 32 ? 0u : ~((1u << valid) - 1u);
-            const uint32_t Lr = (Lc >> 1) | (next_lo << 31) | (beyond >> 1);  // land at x+1
-            const uint32_t Ll = (Lc << 1) | prev_hi;                         // land at x-1
-            const uint32_t coast_bits = Lc & ~(Ll & Lr & Lu & Ld);
-            if (bits) bits[y * words + w] = coast_bits;
-            land += __popc(Lc);
-            coast += __popc(coast_bits);
-            if (mask8) {
-                const int64_t nbit = valid >= 32 ? 32 : valid;
-                for (int b = 0; b < nbit; ++b) mask8[y * R + w * 32 + b] = (coast_bits >> b) & 1u;
-            }
+            Lu = Lc;
+            Lc = Ld;
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -264,7 +270,7 @@ __global__ void boxcount_pow2_kernel(const uint32_t* __restrict__ bits, int64_t 
     const int s = blockIdx.y;
     if (s >= n_sizes) return;
     const int eps = sizes[s];
-    if (!is_pow2_dev(eps)) return;
+    if (!is_pow2_dev(eps) || eps <= 32) return;  // eps <= 32: boxcount_pow2_fused_kernel
     const int64_t words = (R + 31) / 32;
     const int64_t bpy = (rows + eps - 1) / eps;
     unsigned long long occ = 0;
@@ -296,6 +302,57 @@ __global__ void boxcount_pow2_kernel(const uint32_t* __restrict__ bits, int64_t 
     }
     for (int o = 16; o > 0; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
     if ((threadIdx.x & 31) == 0 && occ) atomicAdd(&out[s], occ);
+}
+
+// All power-of-two sides 1..32 in one pass over the bits: a thread owns one
+// word column of a 32-row block, ORs its rows pairwise up the levels
+// (2, 4, 8, 16, 32 rows; the groups are anchored at multiples of eps since the
+// block starts at a multiple of 32), folds each level's OR within the word by
+// eps bits and counts the group leaders.  idx[j] = bit mask of the indices
+// of the size 2^j in the caller's list (n_sizes <= 64).
+struct Pow2Slots {
+    unsigned long long idx[6];
+};
+__global__ void boxcount_pow2_fused_kernel(const uint32_t* __restrict__ bits, int64_t R, int64_t rows,
+                                           const __grid_constant__ Pow2Slots ps, unsigned long long* __restrict__ out) {
+    const int64_t words = (R + 31) / 32;
+    const int64_t blocks_y = (rows + 31) / 32;
+    unsigned long long occ[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < blocks_y * words;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t by = t / words, w = t - by * words;
+        const int64_t y0 = by * 32;
+        const int nr = static_cast<int>(rows - y0 < 32 ? rows - y0 : 32);
+        uint32_t a[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) a[r] = r < nr ? __ldg(bits + (y0 + r) * words + w) : 0u;
+        constexpr uint32_t lead[6] = {0xFFFFFFFFu, 0x55555555u, 0x11111111u, 0x01010101u, 0x00010001u, 1u};
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            const int ng = 32 >> j;  // groups of 2^j rows in the block
+#pragma unroll
+            for (int g = 0; g < 32; ++g) {
+                if (g < ng) {
+                    uint32_t m = a[g];
+#pragma unroll
+                    for (int sh = 1; sh < (1 << j); sh <<= 1) m |= m >> sh;
+                    occ[j] += __popc(m & lead[j]);
+                }
+            }
+            if (j < 5) {
+#pragma unroll
+                for (int g = 0; g < 16; ++g)
+                    if (g < (ng >> 1)) a[g] = a[2 * g] | a[2 * g + 1];
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        unsigned long long v = occ[j];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v)
+            for (unsigned long long m = ps.idx[j]; m; m &= m - 1) atomicAdd(&out[__ffsll(m) - 1], v);
+    }
 }
 
 // Occupied boxes of side eps (partial far-edge boxes count, analysis.hpp:284);
@@ -607,14 +664,17 @@ int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* str
 static int coast_common(const float* dev_map, int64_t R, int64_t rows, int64_t ld, int has_top, int has_bot,
                         double sea, uint32_t* bits, uint8_t* mask8, unsigned long long* counts, cudaStream_t s) {
     const int64_t segs = ((R + 31) / 32 + 31) / 32;
-    const int64_t warps = rows * segs;
+    // strips of up to kCoastRows rows, shorter when the map offers fewer
+    // than ~4 warps of work per SMSP
+    const int srows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kCoastRows, rows * segs / (148 * 16))));
+    const int64_t warps = ((rows + srows - 1) / srows) * segs;
     const int64_t blocks = std::min<int64_t>((warps * 32 + 255) / 256, 148 * 16);
     // land test h >= sea with the fp32 map widened exactly: for a double sea
     // level, h >= sea  <=>  h >= the smallest float >= sea.
     float seaf = static_cast<float>(sea);
     if (static_cast<double>(seaf) < sea) seaf = nextafterf(seaf, INFINITY);
     coast_bits_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(dev_map, R, rows, ld, has_top, has_bot, seaf,
-                                                                     bits, mask8, counts);
+                                                                     srows, bits, mask8, counts);
     return cudaGetLastError() == cudaSuccess ? TG_OK : set_error(TG_EDEVICE, "coastline kernel launch");
 }
 
@@ -636,7 +696,17 @@ static int boxcount_from_bits(const uint32_t* bits, int64_t R, int64_t rows, con
     dim3 grid(148 * 4, static_cast<unsigned>(n));
     bool any_other = false;
     for (int i = 0; i < n; ++i) any_other = any_other || (sizes[i] & (sizes[i] - 1)) != 0;
-    boxcount_pow2_kernel<<<grid, 256, 0, s>>>(bits, R, rows, dsizes, n, dcounts);
+    Pow2Slots ps = {};
+    bool big = false;
+    for (int i = 0; i < n; ++i) {
+        const int v = sizes[i];
+        if (v > 0 && (v & (v - 1)) == 0 && v <= 32)
+            ps.idx[__builtin_ctz(static_cast<unsigned>(v))] |= 1ull << i;
+        else if (v > 32 && (v & (v - 1)) == 0)
+            big = true;
+    }
+    boxcount_pow2_fused_kernel<<<148 * 4, 256, 0, s>>>(bits, R, rows, ps, dcounts);
+    if (big) boxcount_pow2_kernel<<<grid, 256, 0, s>>>(bits, R, rows, dsizes, n, dcounts);
     if (any_other) boxcount_kernel<<<grid, 256, 0, s>>>(bits, R, rows, dsizes, n, dcounts);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "boxcount launch");
