@@ -125,4 +125,52 @@ inline void write_png16(const std::string& path, const float* dev_map, int width
     write_file(path, encode_png16(dev_map, width, height, width));
 }
 
+// 16-bit P5 PGM reader (the reference's read_pgm16, io.hpp:113-160): header
+// tokens (width, height, maxval = 65535) with '#' comment lines anywhere, the
+// "# hmin=... hmax=..." comment giving the height range (default [0, 1]),
+// one whitespace byte, then big-endian samples.
+struct Image16 {
+    int width = 0, height = 0;
+    double hmin = 0.0, hmax = 1.0;
+    std::vector<std::uint16_t> samples;
+    // sample -> height (io.hpp:162-168)
+    double height_of(std::uint32_t s) const { return hmin + static_cast<double>(s) / 65535.0 * (hmax - hmin); }
+};
+
+inline Image16 read_pgm16(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open for reading: " + path);
+    std::string magic;
+    in >> magic;
+    if (magic != "P5") throw IoError("read_pgm16: not a P5 PGM stream");
+    Image16 img;
+    int field[3] = {0, 0, 0};
+    for (int got = 0; got < 3;) {
+        in >> std::ws;
+        if (in.peek() == '#') {
+            std::string line;
+            std::getline(in, line);
+            double lo, hi;
+            if (std::sscanf(line.c_str(), "# hmin=%lf hmax=%lf", &lo, &hi) == 2) {
+                img.hmin = lo;
+                img.hmax = hi;
+            }
+            continue;
+        }
+        if (!(in >> field[got++])) throw IoError("read_pgm16: malformed header");
+    }
+    img.width = field[0];
+    img.height = field[1];
+    if (img.width < 1 || img.height < 1) throw IoError("read_pgm16: bad dimensions");
+    if (field[2] != 65535) throw IoError("read_pgm16: expected 16-bit maxval 65535");
+    in.get();
+    const std::size_t n = static_cast<std::size_t>(img.width) * static_cast<std::size_t>(img.height);
+    std::vector<unsigned char> raw(2 * n);
+    in.read(reinterpret_cast<char*>(raw.data()), static_cast<std::streamsize>(raw.size()));
+    if (in.gcount() != static_cast<std::streamsize>(raw.size())) throw IoError("read_pgm16: truncated pixel data");
+    img.samples.resize(n);
+    for (std::size_t i = 0; i < n; ++i) img.samples[i] = static_cast<std::uint16_t>(raw[2 * i] << 8 | raw[2 * i + 1]);
+    return img;
+}
+
 }  // namespace terrain_b200::io
