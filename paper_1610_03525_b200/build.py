@@ -12,12 +12,13 @@ import os
 import subprocess
 import sys
 import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libpolyterrain_b200.so")
-SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "perm2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu",
+SOURCES = ["capi.cu", "fbm2d.cu", "simplex2d.cu", "perm2d.cu", "fbm3d.cu", "kernels.cu", "analysis.cu", "vgring.cu",
            "hostpipe.cpp", "terrain.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,19 +43,23 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     objdir = tempfile.mkdtemp(prefix="tgobj_", dir=LIB_DIR)  # private: concurrent builds of variants
-    objs = []
-    for src in SOURCES:
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
-            print(" ".join(cmd))
-        out = subprocess.run(cmd, capture_output=True, text=True)
-        if out.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{out.stderr}")
-        if verbose and out.stderr:
-            print(out.stderr)
-        objs.append(obj)
+        return src, obj, cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
+        for src, obj, cmd, out in pool.map(compile_one, SOURCES):
+            if verbose:
+                print(" ".join(cmd))
+            if out.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src}:\n{out.stderr}")
+            if verbose and out.stderr:
+                print(out.stderr)
+            objs.append(obj)
     os.makedirs(os.path.dirname(target), exist_ok=True)
     tmp = target + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lpthread", "-ldl"]

@@ -615,6 +615,11 @@ variogram_y_kernel(const float* __restrict__ z, int64_t W, int64_t H, int64_t ld
     }
 }
 
+}  // namespace
+int vg_ring_enqueue(const float* z, int64_t W, int64_t H, int64_t ld, int64_t P, const int32_t* lags, int n_lags,
+                    double* sums, int sm, cudaStream_t s, cudaStream_t sy);
+namespace {
+
 struct Scratch {
     void* p = nullptr;
     cudaStream_t s;
@@ -887,7 +892,10 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
         }
     }
     const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dev_map) & 15) == 0;
-    for (int l0 = 0; l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += kFusedLags) {
+    // power-of-two lags up to 4096 (config 5's set): register-ring walks (vgring.cu)
+    const int ring = vg_ring_enqueue(dev_map, width, height, ld, pair_rows, lags, n_lags, sums, sm, s, sy);
+    if (ring < 0) return ring;
+    for (int l0 = 0; ring && l0 < n_lags && e == cudaSuccess && pair_rows > 0; l0 += kFusedLags) {
         const int n = std::min(kFusedLags, n_lags - l0);
         LagSet Lx{}, Ly{};
         Lx.n = Ly.n = n;
@@ -920,6 +928,13 @@ int tg_variogram_band_f32(const float* dev_map, int64_t width, int64_t height, i
     if (e == cudaSuccess) e = cudaMemcpyAsync(out_sum_sq, sums, 2 * n_lags * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return set_cuda_error(e, "variogram");
+    for (int i = 0; ring == 0 && i < n_lags; ++i)  // the ring path sums a repeated lag once
+        for (int j = 0; j < i; ++j)
+            if (lags[j] == lags[i]) {
+                out_sum_sq[2 * i] = out_sum_sq[2 * j];
+                out_sum_sq[2 * i + 1] = out_sum_sq[2 * j + 1];
+                break;
+            }
     for (int i = 0; i < n_lags; ++i) {
         const int64_t h = lags[i];
         out_pairs[2 * i] = h < width ? (width - h) * pair_rows : 0;
