@@ -16,6 +16,7 @@
 
 #include "../../include/polyterrain_b200.h"
 #include "devattr.h"
+#include "select.h"
 
 namespace tg {
 int set_error(int code, const char* msg);
@@ -54,6 +55,30 @@ __device__ __forceinline__ void hist_flush(const unsigned int* sh, unsigned long
     __syncthreads();
     for (int i = threadIdx.x; i < kBins; i += blockDim.x)
         if (sh[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(sh[i]));
+}
+
+// Neighbouring heights share digits, so a warp's keys pile onto a few bins and
+// plain shared atomics serialise on equal addresses.  Each thread merges its
+// batch into runs of equal bins; the last run of every lane goes in as ONE
+// atomic when the whole warp's last runs share a bin (the common case on a
+// smooth map), else one atomic per lane.  All 32 lanes must call it.
+template <int N>
+__device__ __forceinline__ void hist_runs(unsigned int* sh, const uint32_t (&bin)[N], const bool (&ok)[N]) {
+    uint32_t cur = 0xffffffffu, cnt = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {  // branch-free bookkeeping; the flush is one predicated atomic
+        const bool flush = ok[i] && bin[i] != cur && cnt != 0;
+        if (flush) atomicAdd(&sh[cur], cnt);
+        cnt = ok[i] ? (bin[i] == cur ? cnt + 1 : 1) : cnt;
+        cur = ok[i] ? bin[i] : cur;
+    }
+    const uint32_t b0 = __shfl_sync(0xffffffffu, cur, 0);
+    if (__all_sync(0xffffffffu, cnt == 0 || cur == b0)) {
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+        if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&sh[b0], tot);
+    } else if (cnt) {
+        atomicAdd(&sh[cur], cnt);
+    }
 }
 
 __global__ void radix_hist(const float* __restrict__ x, uint64_t n, const SelectState* st,
@@ -142,6 +167,213 @@ __global__ void __launch_bounds__(kBins / 2) radix_pick(SelectState* st, unsigne
     }
     if (2 * t < kBins) hist[2 * t] = 0;
     if (2 * t + 1 < kBins) hist[2 * t + 1] = 0;
+}
+
+// ---- radix select with a sampled candidate window -----------------------------
+// Three full histogram passes cost three reads of the map.  Instead the first
+// pass also compacts every key whose first digit lies in a window of digits
+// predicted from a strided sample (the sample's ranks rank_frac +- delta), and
+// the second and third passes histogram only those keys when the selected
+// first digit falls inside the window (otherwise they read the map again:
+// the result is exact either way).  1 read + ~1 % writes instead of 3 reads.
+__device__ __forceinline__ uint32_t d1(uint32_t key) { return key >> 21; }  // first digit (11 bits)
+
+// Top-digit histogram of n_s samples, one at a hashed position in each stride
+// of `step` linear positions (row-major, width w, pitch ld).
+__global__ void sample_hist(const float* __restrict__ x, int64_t width, int64_t ld, uint64_t step, int n_s,
+                            unsigned long long* __restrict__ hist) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_s; j += gridDim.x * blockDim.x) {
+        // j-th stride with a hashed offset inside it (a plain stride samples a
+        // few columns only when it divides the width)
+        const uint64_t p = j * step + (static_cast<uint32_t>(j) * 2654435761u) % step;
+        const int64_t y = static_cast<int64_t>(p / width), c = static_cast<int64_t>(p - y * width);
+        atomicAdd(&hist[d1(fkey(x[y * ld + c]))], 1ull);
+    }
+}
+
+// Pass 1: first-digit histogram of every key; keys with d1 in [wlo, whi] are
+// appended to this block's own segment of keys (seg entries; a warp-aggregated
+// shared-memory counter; writes stop at seg, the count goes on) — one global
+// store of the count per block, no global atomics on a shared counter.
+__device__ __forceinline__ void keep_key(unsigned int* scnt, uint32_t key, uint32_t wlo, uint32_t whi,
+                                         uint32_t* __restrict__ out, uint64_t seg, bool active) {
+    const uint32_t d = d1(key);
+    const bool in = active && d - wlo <= whi - wlo;
+    const uint32_t b = __ballot_sync(0xffffffffu, in);
+    if (b) {
+        const int lane = threadIdx.x & 31;
+        unsigned int base = 0;
+        if (lane == __ffs(b) - 1) base = atomicAdd(scnt, static_cast<unsigned int>(__popc(b)));
+        base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+        const uint64_t at = base + __popc(b & ((1u << lane) - 1u));
+        if (in && at < seg) out[at] = key;
+    }
+}
+
+__global__ void __launch_bounds__(512) radix_hist_keep(const float* __restrict__ x, int64_t width, int64_t rows,
+                                                       int64_t ld, bool vec, uint32_t wlo, uint32_t whi,
+                                                       uint32_t* __restrict__ keys, uint64_t seg,
+                                                       unsigned long long* __restrict__ bcnt,
+                                                       unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[kBins];
+    __shared__ unsigned int scnt;
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+    if (threadIdx.x == 0) scnt = 0;
+    __syncthreads();
+    uint32_t* out = keys + blockIdx.x * seg;
+    if (vec) {  // 16-byte loads (ld and width multiples of 4, aligned base)
+        const int64_t w4 = width / 4, n4 = w4 * rows;
+        const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        // every lane of a warp iterates the same number of times (ballots need the whole warp)
+        const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31);
+        constexpr int kV = 2;  // 16-byte loads in flight per thread
+        const int lane = threadIdx.x & 31;
+        for (int64_t ib = i0; ib < n4; ib += kV * stride) {
+            uint32_t k[4 * kV];
+            bool ok[4 * kV];
+#pragma unroll
+            for (int q = 0; q < kV; ++q) {
+                const int64_t i = ib + q * stride + lane;
+                const bool act = i < n4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (act) {
+                    if (ld == width) {  // contiguous rows: linear index (no 64-bit division per load)
+                        v = __ldg(reinterpret_cast<const float4*>(x) + i);
+                    } else {
+                        const int64_t y = i / w4, c = i - y * w4;
+                        v = __ldg(reinterpret_cast<const float4*>(x + y * ld) + c);
+                    }
+                }
+                k[4 * q] = fkey(v.x), k[4 * q + 1] = fkey(v.y), k[4 * q + 2] = fkey(v.z), k[4 * q + 3] = fkey(v.w);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) ok[4 * q + e] = act;
+            }
+            int mine = 0;
+#pragma unroll
+            for (int e = 0; e < 4 * kV; ++e) {
+                if (ok[e]) atomicAdd(&sh[d1(k[e])], 1u);
+                mine += (ok[e] && d1(k[e]) - wlo <= whi - wlo) ? 1 : 0;
+            }
+            // one shared atomic per warp for its kept keys, lane offsets by a warp scan
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (tot) {
+                unsigned int base = 0;
+                if (lane == 31) base = atomicAdd(&scnt, static_cast<unsigned int>(tot));
+                base = __shfl_sync(0xffffffffu, base, 31);
+                uint64_t at = base + static_cast<unsigned int>(incl - mine);
+#pragma unroll
+                for (int e = 0; e < 4 * kV; ++e)
+                    if (ok[e] && d1(k[e]) - wlo <= whi - wlo) {
+                        if (at < seg) out[at] = k[e];
+                        ++at;
+                    }
+            }
+        }
+    } else {
+        for (int64_t y = blockIdx.x; y < rows; y += gridDim.x)
+            for (int64_t i0 = threadIdx.x & ~int64_t(31); i0 < width; i0 += blockDim.x) {
+                const int64_t i = i0 + (threadIdx.x & 31);
+                const bool act = i < width;
+                const uint32_t k[1] = {act ? fkey(x[y * ld + i]) : 0u};
+                const uint32_t b[1] = {d1(k[0])};
+                const bool ok[1] = {act};
+                hist_runs(sh, b, ok);
+                keep_key(&scnt, k[0], wlo, whi, out, seg, act);
+            }
+    }
+    hist_flush(sh, hist);
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = scnt;
+}
+
+// Contiguous form of radix_hist_keep (ld == width, 16-byte aligned, n % 4 ==
+// 0): the radix_hist loop (two 16-byte loads in flight, no per-key range
+// tests in full iterations) plus the candidate compaction.
+template <bool kTail>
+__device__ __forceinline__ void keep8(unsigned int* sh, unsigned int* scnt, const float4 v, const float4 u, bool a0,
+                                      bool a1, uint32_t wlo, uint32_t whi, uint32_t* __restrict__ out, uint64_t seg) {
+    const uint32_t k[8] = {fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w), fkey(u.x), fkey(u.y), fkey(u.z), fkey(u.w)};
+    int mine = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const bool ok = !kTail || (e < 4 ? a0 : a1);
+        if (ok) atomicAdd(&sh[d1(k[e])], 1u);
+        mine += (ok && d1(k[e]) - wlo <= whi - wlo) ? 1 : 0;
+    }
+    if (__any_sync(0xffffffffu, mine != 0)) {  // rare: a warp with candidates
+        const int lane = threadIdx.x & 31;
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        unsigned int base = 0;
+        if (lane == 31) base = atomicAdd(scnt, static_cast<unsigned int>(incl));
+        base = __shfl_sync(0xffffffffu, base, 31);
+        uint64_t at = base + static_cast<unsigned int>(incl - mine);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if ((!kTail || (e < 4 ? a0 : a1)) && d1(k[e]) - wlo <= whi - wlo) {
+                if (at < seg) out[at] = k[e];
+                ++at;
+            }
+    }
+}
+
+__global__ void __launch_bounds__(512) radix_hist_keep_lin(const float4* __restrict__ x4, uint64_t n4, uint32_t wlo,
+                                                           uint32_t whi, uint32_t* __restrict__ keys, uint64_t seg,
+                                                           unsigned long long* __restrict__ bcnt,
+                                                           unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[kBins];
+    __shared__ unsigned int scnt;
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+    if (threadIdx.x == 0) scnt = 0;
+    __syncthreads();
+    uint32_t* out = keys + blockIdx.x * seg;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t lane = threadIdx.x & 31;
+    uint64_t ib = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u);
+    for (; ib + stride + 32 <= n4; ib += 2 * stride)  // whole warps, both loads in range
+        keep8<false>(sh, &scnt, __ldg(x4 + ib + lane), __ldg(x4 + ib + stride + lane), true, true, wlo, whi, out, seg);
+    for (; ib < n4; ib += 2 * stride) {  // warp-uniform tail
+        const uint64_t i = ib + lane, j = i + stride;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        keep8<true>(sh, &scnt, i < n4 ? __ldg(x4 + i) : z, j < n4 ? __ldg(x4 + j) : z, i < n4, j < n4, wlo, whi, out,
+                    seg);
+    }
+    hist_flush(sh, hist);
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = scnt;
+}
+
+// Passes 2 and 3 over the kept keys (block b reads segment b).
+__global__ void radix_hist_keys(const uint32_t* __restrict__ keys, uint64_t seg, const unsigned long long* bcnt,
+                                uint32_t prefix, uint32_t mask, int shift, int bits,
+                                unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[kBins];
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint64_t n = bcnt[blockIdx.x];
+    const uint32_t* in = keys + blockIdx.x * seg;
+    const uint32_t dmask = (1u << bits) - 1u;
+    for (uint64_t i0 = 0; i0 < n; i0 += 8 * blockDim.x) {  // 8 consecutive kept keys per thread
+        const uint64_t i = i0 + 8 * threadIdx.x;
+        uint32_t b[8];
+        bool ok[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t k = i + e < n ? in[i + e] : 0u;
+            b[e] = (k >> shift) & dmask;
+            ok[e] = i + e < n && (k & mask) == prefix;
+        }
+        hist_runs(sh, b, ok);
+    }
+    hist_flush(sh, hist);
 }
 
 // ---- coastline bit mask -------------------------------------------------------
@@ -631,6 +863,129 @@ struct Scratch {
 };
 
 }  // namespace
+
+// One pass of the (possibly distributed) upper-median radix select over a
+// window (width x rows, pitch ld): the digit histogram (shift, bits) of the
+// keys matching prefix/mask, to the host.  With a cache, the first pass
+// (mask == 0) also keeps a candidate window of keys (see radix_hist_keep) and
+// later passes read only those when the chosen first digit lies inside it.
+int select_hist(const float* map, int64_t width, int64_t rows, int64_t ld, uint32_t prefix, uint32_t mask, int shift,
+                int bits, uint64_t* out_hist, SelectCache* cache, cudaStream_t s) {
+    const uint64_t n = static_cast<uint64_t>(width) * static_cast<uint64_t>(rows);
+    const size_t hb = kBins * sizeof(unsigned long long);
+    if (cache && cache->dev_hist == nullptr) {
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&cache->dev_hist), hb + 64, s);
+        if (e != cudaSuccess) return set_cuda_error(e, "select alloc");
+    }
+    Scratch scr(s);
+    unsigned long long* hist = nullptr;
+    unsigned long long* cnt = nullptr;
+    if (cache) {
+        hist = cache->dev_hist;
+        cnt = hist + kBins;
+    } else {
+        cudaError_t e = scr.alloc(hb + 64);
+        if (e != cudaSuccess) return set_cuda_error(e, "select alloc");
+        hist = static_cast<unsigned long long*>(scr.p);
+        cnt = hist + kBins;
+    }
+    cudaError_t e = cudaMemsetAsync(hist, 0, hb + 8, s);
+    const bool vec = (ld & 3) == 0 && (width & 3) == 0 && (reinterpret_cast<uintptr_t>(map) & 15) == 0;
+    const int hblocks = static_cast<int>(std::min<int64_t>(std::max<int64_t>(rows, 1), kHistBlocks));
+    if (cache && mask == 0 && shift == 21 && bits == 11 && n >= (uint64_t(1) << 22)) {
+        // window of first digits from a strided sample of 2^18 keys
+        constexpr int kS = 1 << 18;
+        std::vector<unsigned long long> sh(kBins);
+        if (e == cudaSuccess) sample_hist<<<128, 512, 0, s>>>(map, width, ld, n / kS, kS, hist);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sh.data(), hist, hb, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return set_cuda_error(e, "select sample");
+        const double lo = (cache->rank_frac - cache->delta) * kS, hi = (cache->rank_frac + cache->delta) * kS;
+        uint64_t c = 0;
+        int wlo = -1, whi = -1;
+        for (int d = 0; d < kBins; ++d) {
+            const uint64_t c1 = c + sh[d];
+            if (wlo < 0 && static_cast<double>(c1) > lo) wlo = d;
+            if (whi < 0 && static_cast<double>(c1) > hi) whi = d;
+            c = c1;
+        }
+        if (wlo < 0) wlo = kBins - 1;
+        if (whi < 0) whi = kBins - 1;
+        uint64_t in = 0;
+        for (int d = wlo; d <= whi; ++d) in += sh[d];
+        // twice the expected window count (blocks see near-equal shares of it)
+        const uint64_t cap = static_cast<uint64_t>(2.0 * static_cast<double>(in + 64) / kS * static_cast<double>(n)) +
+                             (uint64_t(1) << 20);
+        cache->valid = false;
+        if (static_cast<double>(in) / kS <= 0.3) {
+            if (cache->cap < cap) {
+                if (cache->keys) cudaFreeAsync(cache->keys, s);
+                cache->keys = nullptr;
+                cache->cap = 0;
+                e = cudaMallocAsync(reinterpret_cast<void**>(&cache->keys), cap * sizeof(uint32_t), s);
+                if (e != cudaSuccess) return set_cuda_error(e, "select keys alloc");
+                cache->cap = cap;
+            }
+            cache->wlo = static_cast<uint32_t>(wlo);
+            cache->whi = static_cast<uint32_t>(whi);
+            if (!cache->bcnt) {
+                e = cudaMallocAsync(reinterpret_cast<void**>(&cache->bcnt), kHistBlocks * sizeof(unsigned long long), s);
+                if (e != cudaSuccess) return set_cuda_error(e, "select counts alloc");
+            }
+            const uint64_t seg = cache->cap / kHistBlocks;
+            e = cudaMemsetAsync(hist, 0, hb + 8, s);
+            if (e == cudaSuccess) {
+                if (vec && ld == width)
+                    radix_hist_keep_lin<<<kHistBlocks, 512, 0, s>>>(reinterpret_cast<const float4*>(map), n / 4,
+                                                                    cache->wlo, cache->whi, cache->keys, seg,
+                                                                    cache->bcnt, hist);
+                else
+                    radix_hist_keep<<<kHistBlocks, 512, 0, s>>>(map, width, rows, ld, vec, cache->wlo, cache->whi,
+                                                               cache->keys, seg, cache->bcnt, hist);
+            }
+            std::vector<unsigned long long> got(kHistBlocks);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaMemcpyAsync(out_hist, hist, hb, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(got.data(), cache->bcnt, kHistBlocks * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return set_cuda_error(e, "select pass 1");
+            cache->valid = true;
+            for (auto g : got) cache->valid = cache->valid && g <= seg;
+            return TG_OK;
+        }
+    }
+    const bool from_keys = cache && cache->valid && (mask & 0xffe00000u) == 0xffe00000u &&
+                           (prefix >> 21) - cache->wlo <= cache->whi - cache->wlo;
+    if (e == cudaSuccess) {
+        SelectState init{prefix, mask, 0};
+        SelectState* st = reinterpret_cast<SelectState*>(cnt + 1);  // 64 spare bytes after the histogram
+        e = cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            if (from_keys)
+                radix_hist_keys<<<kHistBlocks, 512, 0, s>>>(cache->keys, cache->cap / kHistBlocks, cache->bcnt, prefix,
+                                                            mask, shift, bits, hist);
+            else if (ld == width)
+                radix_hist<<<kHistBlocks, 512, 0, s>>>(map, n, st, shift, bits, hist);
+            else
+                radix_hist2d<<<hblocks, 512, 0, s>>>(map, width, rows, ld, st, shift, bits, hist);
+            e = cudaGetLastError();
+        }
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_hist, hist, (size_t{1} << bits) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_cuda_error(e, "select histogram");
+    return TG_OK;
+}
+
+void select_cache_free(SelectCache* c, cudaStream_t s) {
+    if (c->keys) cudaFreeAsync(c->keys, s);
+    if (c->bcnt) cudaFreeAsync(c->bcnt, s);
+    if (c->dev_hist) cudaFreeAsync(c->dev_hist, s);
+    *c = SelectCache{};
+}
+
 }  // namespace tg
 
 using namespace tg;
@@ -642,26 +997,40 @@ int tg_median_f32(const float* dev_map, uint64_t n, float* out_median, void* str
         return set_error(TG_EVALIDATION, "coastline_mask: empty heightmap");
     if (int st = check_device()) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Scratch scr(s);
-    cudaError_t e = scr.alloc(64 + kBins * sizeof(unsigned long long));
-    if (e != cudaSuccess) return set_cuda_error(e, "median alloc");
-    SelectState* state = static_cast<SelectState*>(scr.p);
-    unsigned long long* hist = reinterpret_cast<unsigned long long*>(static_cast<char*>(scr.p) + 64);
-    SelectState init{0u, 0u, n / 2};  // analysis.hpp:247 (upper median)
-    e = cudaMemcpyAsync(state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned long long), s);
-    const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
-    for (int p = 0; p < 3 && e == cudaSuccess; ++p) {
-        radix_hist<<<kHistBlocks, 512, 0, s>>>(dev_map, n, state, shifts[p], widths[p], hist);
-        radix_pick<<<1, kBins / 2, 0, s>>>(state, hist, shifts[p], widths[p]);
-        e = cudaGetLastError();
+    // the map as rows of up to 2^20 keys (any n), ragged tail as its own window
+    const int64_t W = n >= (uint64_t(1) << 20) ? (int64_t(1) << 20) : static_cast<int64_t>(n);
+    const int64_t rows = static_cast<int64_t>(n / W), tail = static_cast<int64_t>(n - uint64_t(rows) * W);
+    SelectCache cache;
+    uint32_t prefix = 0, mask = 0;
+    uint64_t k = n / 2;  // analysis.hpp:247 (upper median)
+    const int digits[3][2] = {{21, 11}, {10, 11}, {0, 10}};
+    std::vector<uint64_t> h(kBins), ht(kBins);
+    int st = TG_OK;
+    for (const auto& dg : digits) {
+        const int shift = dg[0], bits = dg[1];
+        st = select_hist(dev_map, W, rows, W, prefix, mask, shift, bits, h.data(), &cache, s);
+        if (st == TG_OK && tail)
+            st = select_hist(dev_map + uint64_t(rows) * W, tail, 1, tail, prefix, mask, shift, bits, ht.data(), nullptr,
+                             s);
+        if (st != TG_OK) break;
+        uint64_t c = 0;
+        int d = 0;
+        for (; d < (1 << bits); ++d) {
+            const uint64_t hd = h[d] + (tail ? ht[d] : 0);
+            if (c + hd > k) break;
+            c += hd;
+        }
+        if (d == (1 << bits)) {
+            st = set_error(TG_ENUMERICAL, "median: select out of range");
+            break;
+        }
+        k -= c;
+        prefix |= static_cast<uint32_t>(d) << shift;
+        mask |= ((1u << bits) - 1u) << shift;
     }
-    SelectState res{};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&res, state, sizeof(res), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return set_cuda_error(e, "median");
-    const uint32_t k = res.prefix;
-    const uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    select_cache_free(&cache, s);
+    if (st != TG_OK) return st;
+    const uint32_t b = (prefix & 0x80000000u) ? (prefix & 0x7fffffffu) : ~prefix;
     std::memcpy(out_median, &b, 4);
     return TG_OK;
 }

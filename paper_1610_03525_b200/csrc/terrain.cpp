@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "../../include/polyterrain_b200.h"
+#include "select.h"
 
 namespace tg {
 int set_error(int code, const char* msg);
@@ -137,6 +138,7 @@ struct DeviceBand {
     const tg_band* b;
     float* buf = nullptr;  // gen rows x width, contiguous
     cudaStream_t st;
+    tg::SelectCache sel;   // candidate keys kept by the first median pass
 
     const float* owned() const { return buf + b->halo_top * t->width; }
     bool last() const { return b->y0 - t->y_origin + b->rows >= t->height; }
@@ -180,7 +182,10 @@ int dev_generate(void* ctx, const tg_band* b) {
 }
 int dev_histogram(void* ctx, uint32_t prefix, uint32_t mask, int32_t shift, int32_t bits, uint64_t* hist) {
     auto* d = static_cast<DeviceBand*>(ctx);
-    return tg_histogram_f32(d->owned(), d->t->width, d->b->rows, d->t->width, prefix, mask, shift, bits, hist, d->st);
+    if (bits < 1 || bits > 11 || shift < 0 || shift + bits > 32)
+        return tg::set_error(TG_EVALIDATION, "histogram: bad arguments");
+    return tg::select_hist(d->owned(), d->t->width, d->b->rows, d->t->width, prefix, mask, shift, bits, hist, &d->sel,
+                           d->st);
 }
 int dev_boxcount(void* ctx, double sea, const int32_t* sizes, int32_t n, int64_t* counts, int64_t* coast,
                  int64_t* land) {
@@ -430,8 +435,13 @@ int tg_terrain_stats_band(const tg_fbm_config* cfg, const tg_terrain* t, const t
     if (!cfg || !t || !b) return tg::set_error(TG_EVALIDATION, "terrain_stats: null argument");
     if (int st = tg::check_device()) return st;
     DeviceBand d{cfg, t, b, nullptr, static_cast<cudaStream_t>(stream)};
+    // one band: the local median is the global one (narrow candidate window);
+    // several: the global median's local rank is unknown (wide window)
+    d.sel.delta = comm && comm->nranks > 1 ? 0.05 : 0.005;
     tg_band_ops ops{&d, dev_generate, dev_histogram, dev_boxcount, dev_variogram};
-    return tg_terrain_stats_ops(t, b, sizes, n_sizes, lags, n_lags, sea_level, comm, &ops, out);
+    const int st = tg_terrain_stats_ops(t, b, sizes, n_sizes, lags, n_lags, sea_level, comm, &ops, out);
+    tg::select_cache_free(&d.sel, d.st);
+    return st;
 }
 
 }  // extern "C"

@@ -53,9 +53,9 @@ def phases(lib, world, rank):
 
     t("regenerate_band_ms", lambda: lib.tg_fbm_generate_rect_f32(C.byref(c), 0, band.gen_y0, T, band.gen_rows,
                                                                  buf.data_ptr(), T, None))
-    hist = np.zeros(2048, dtype=np.uint64)
-    t("median_histograms_ms", lambda: [lib.tg_histogram_f32(own, T, band.rows, T, 0, 0, sh, bits, hist.ctypes.data,
-                                                            None) for sh, bits in ((21, 11), (10, 11), (0, 10))])
+    med = C.c_float()
+    # the band's own upper median (the radix select with the sampled candidate window)
+    t("median_ms", lambda: lib.tg_median_f32(own, T * band.rows, C.byref(med), None))
     sz = (C.c_int32 * 6)(2, 4, 8, 16, 32, 64)
     cnt = (C.c_int64 * 6)()
     a, b = C.c_int64(), C.c_int64()
