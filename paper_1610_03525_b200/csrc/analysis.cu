@@ -389,28 +389,33 @@ __global__ void radix_hist_keys(const uint32_t* __restrict__ keys, uint64_t seg,
 // regenerated by the caller for row-band shards.
 constexpr int kCoastRows = 32;
 
-// Land word of lane's w = w0 + lane in `row` (x >= R: not land).
-__device__ __forceinline__ uint32_t land_word(const float* __restrict__ row, int64_t w0, int64_t R, float sea,
-                                              int lane) {
+// Land word of lane's w = w0 + lane in `row` (x >= R: not land), split into
+// the 32 loads (issued one row ahead) and the 32 ballots.
+__device__ __forceinline__ void land_load(const float* __restrict__ row, int64_t w0, int64_t R, int lane,
+                                          float (&v)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int64_t x = (w0 + i) * 32 + lane;
+        v[i] = x < R ? __ldg(row + x) : -INFINITY;
+    }
+}
+__device__ __forceinline__ uint32_t land_bits(const float (&v)[32], float sea, int lane) {
     uint32_t L = 0;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {  // all 16 loads of a half in flight before the ballots
-            const int64_t x = (w0 + 16 * half + i) * 32 + lane;
-            v[i] = x < R ? row[x] : -INFINITY;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t b = __ballot_sync(0xffffffffu, v[i] >= sea);
-            if (lane == 16 * half + i) L = b;
-        }
+    for (int i = 0; i < 32; ++i) {
+        const uint32_t b = __ballot_sync(0xffffffffu, v[i] >= sea);
+        if (lane == i) L = b;
     }
     return L;
 }
 
-__global__ void __launch_bounds__(256, 4)
+// The 32 loads of the next row are in flight while the current row's coast
+// bits are formed (the latency of one row per warp was the bound: 80 %
+// long-scoreboard stalls with the loads issued row by row).
+#ifndef TG_COAST_MINB
+#define TG_COAST_MINB 3
+#endif
+__global__ void __launch_bounds__(256, TG_COAST_MINB)
 coast_bits_kernel(const float* __restrict__ h, int64_t R, int64_t rows, int64_t ld,
                                   int has_top, int has_bot, float sea, int srows,
                                   uint32_t* __restrict__ bits, uint8_t* __restrict__ mask8,
@@ -422,6 +427,7 @@ coast_bits_kernel(const float* __restrict__ h, int64_t R, int64_t rows, int64_t 
     const int64_t warp_global = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long land = 0, coast = 0;
+    float v[32];
     for (int64_t t = warp_global; t < strips * segs; t += nwarps) {
         const int64_t st = t / segs;
         const int64_t w0 = (t - st * segs) * 32;
@@ -429,11 +435,20 @@ coast_bits_kernel(const float* __restrict__ h, int64_t R, int64_t rows, int64_t 
         const int64_t w = w0 + lane;
         const int64_t valid = R - w * 32;  // bits beyond R count as land for the horizontal test
         const uint32_t beyond = valid >= 32 ? 0u : ~((1u << (valid > 0 ? valid : 0)) - 1u);
-        uint32_t Lu = (y0 > 0 || has_top) ? land_word(h + (y0 - 1) * ld, w0, R, sea, lane) : 0xffffffffu;
-        uint32_t Lc = land_word(h + y0 * ld, w0, R, sea, lane);
+        uint32_t Lu = 0xffffffffu;
+        if (y0 > 0 || has_top) {
+            land_load(h + (y0 - 1) * ld, w0, R, lane, v);
+            Lu = land_bits(v, sea, lane);
+        }
+        land_load(h + y0 * ld, w0, R, lane, v);
+        uint32_t Lc = land_bits(v, sea, lane);
+        const bool more0 = y0 + 1 < rows || has_bot;
+        if (more0) land_load(h + (y0 + 1) * ld, w0, R, lane, v);
         for (int64_t y = y0; y < y1; ++y) {
             const float* row = h + y * ld;
-            const uint32_t Ld = (y + 1 < rows || has_bot) ? land_word(row + ld, w0, R, sea, lane) : 0xffffffffu;
+            const bool more = y + 1 < rows || has_bot;
+            const uint32_t Ld = more ? land_bits(v, sea, lane) : 0xffffffffu;
+            if (y + 1 < y1 && (y + 2 < rows || has_bot)) land_load(row + 2 * ld, w0, R, lane, v);  // next row in flight
             // horizontal neighbours: bit b-1 / b+1 incl. the adjacent words' edge bits
             const uint32_t prev = __shfl_up_sync(0xffffffffu, Lc, 1);
             const uint32_t next = __shfl_down_sync(0xffffffffu, Lc, 1);
