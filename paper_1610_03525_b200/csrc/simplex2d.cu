@@ -10,8 +10,9 @@
 // TG_LANE_SIMPLEX), so chunks stay stateless like every other method.  Sample
 // positions are u = (g + 0.5) * (freq / R) (render_general's position,
 // fbm.hpp:468, with the ratio formed once per octave).
-// Skew, floor and region decisions run in fp64 (as the oracle), the four
-// contributions in fp32.  256 threads x 4 x 8 pixels, one fp32 store.
+// Lattice selection (skew, floors, region) in fp64 with the oracle's
+// operations, the four contributions in fp32.  256 threads x 4 x 8 pixels,
+// octaves outermost, one fp32 store per pixel.
 // Coarse octaves read gradient indices from a per-CTA shared-memory table of
 // every vertex the tile can touch (hashed once per CTA); fine octaves hash
 // per lookup.  Both give the same index, so the choice never changes a pixel.
@@ -41,28 +42,16 @@ __device__ __forceinline__ int exact_int32(double v) {
     return __double2loint(v + 6755399441055744.0);
 }
 
-// Hashes on demand (fine octaves: more vertices than pixels in a tile).
-struct HashGrad {
+// Gradient index of vertex (xsb + a, ysb + b): per-CTA table row / hash.
+struct TableRow {
+    const uint8_t* row0;
+    int nx;
+    __device__ __forceinline__ uint32_t operator()(int a, int b) const { return row0[b * nx + a]; }
+};
+struct HashVtx {
     uint64_t base;
     int64_t xb, yb;
-    __device__ __forceinline__ HashGrad(uint64_t b, double xbd, double ybd) {
-        base = b;
-        xb = __double2ll_rd(xbd);
-        yb = __double2ll_rd(ybd);
-    }
     __device__ __forceinline__ uint32_t operator()(int a, int b) const { return grad_index(base, xb + a, yb + b); }
-};
-
-// Per-CTA table of the gradient indices of every vertex the tile can touch
-// (coarse octaves: a few vertices shared by many pixels), filled once.
-struct TableGrad {
-    const uint8_t* row0;  // entry of vertex (xsb, ysb)
-    int nx;
-    __device__ __forceinline__ TableGrad(const uint8_t* t, int n, double bx, double by, double xbd, double ybd) {
-        row0 = t + exact_int32(ybd - by) * n + exact_int32(xbd - bx);
-        nx = n;
-    }
-    __device__ __forceinline__ uint32_t operator()(int a, int b) const { return row0[b * nx + a]; }
 };
 
 // (2 - d^2)^4 (g . d) for the vertex at offset (a, b) from (xsb, ysb):
@@ -78,39 +67,6 @@ __device__ __forceinline__ float contrib(const G& grad, const float2* gv, int a,
     const float2 g = gv[grad(a, b)];
     attn *= attn;
     return attn * attn * fmaf(g.x, dx, g.y * dy);
-}
-
-// Skew, floor and region decisions in fp64 (the oracle's order of
-// operations); contributions in fp32, summed in the order v1, v2, v3, extra.
-template <class G>
-__device__ __forceinline__ float opensimplex(const G& grad, const float2* gv, double x, double y,
-                                             double xb, double yb, double xs, double ys) {
-    const double sq = (xb + yb) * kSquish;
-    const double xins = xs - xb, yins = ys - yb;
-    const double in_sum = xins + yins;
-    const float dx0 = static_cast<float>(x - (xb + sq));
-    const float dy0 = static_cast<float>(y - (yb + sq));
-    const bool upper = in_sum > 1.0;
-    // v3 = (c, c); extra vertex (ea, eb)
-    int ea, eb;
-    if (!upper) {
-        const double zins = 1.0 - in_sum;
-        const bool edge = zins > xins || zins > yins;
-        ea = edge ? (xins > yins ? 1 : -1) : 1;
-        eb = edge ? (xins > yins ? -1 : 1) : 1;
-    } else {
-        const double zins = 2.0 - in_sum;
-        const bool edge = zins < xins || zins < yins;
-        ea = edge ? (xins > yins ? 2 : 0) : 0;
-        eb = edge ? (xins > yins ? 0 : 2) : 0;
-    }
-    const int c = upper ? 1 : 0;
-    const float fc = upper ? 1.0f : 0.0f;
-    float v = contrib(grad, gv, 1, 0, 1.0f, 0.0f, dx0, dy0);
-    v += contrib(grad, gv, 0, 1, 0.0f, 1.0f, dx0, dy0);
-    v += contrib(grad, gv, c, c, fc, fc, dx0, dy0);
-    v += contrib(grad, gv, ea, eb, static_cast<float>(ea), static_cast<float>(eb), dx0, dy0);
-    return v * (1.0f / 47.0f);
 }
 
 constexpr int kTW = 128, kTH = 64, kThreads = 256;
@@ -129,6 +85,63 @@ __host__ __device__ inline void table_dims(double fr, int* nx, int* ny) {
 struct TabPlan {
     double bx, by;  // table origin (integral)
 };
+
+// One octave for 4 consecutive pixels of a row (rows and octaves are rolled
+// loops around it: one unrolled body per mode keeps the kernel small — the
+// fully unrolled 4 x 8 body stalled 44 % on instruction fetch).
+// Lattice selection in fp64 with the oracle's operations (u, v, the skew, the
+// two floors, xins / yins / in_sum and the region comparisons), so every pixel
+// picks the oracle's vertices; the offsets from the cell origin in fp32 via
+// dx0 = xins + in_sum * squish (the oracle's x - (xsb + (xsb + ysb) squish)).
+template <bool kTable>
+__device__ __forceinline__ void os_octave4(float (&acc)[4], const float2* gv, double fr, float amp,
+                                           const uint8_t* tab, int nx, double bx, double by, uint64_t base,
+                                           const double (&gx)[4], double gy) {
+    constexpr float S = static_cast<float>(kSquish);
+    const double v = __dmul_rn(gy, fr);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double u = __dmul_rn(gx[j], fr);
+        const double so = (u + v) * kStretch;
+        const double xs = u + so, ys = v + so;
+        const double xb = floor(xs), yb = floor(ys);
+        const double xins = xs - xb, yins = ys - yb;
+        const double in_sum = xins + yins;
+        const bool upper = in_sum > 1.0;
+        const double zins = (upper ? 2.0 : 1.0) - in_sum;
+        // branch-free region: the four comparisons, then selects (a divergent
+        // branch per pixel cost both paths)
+        const bool gtx = zins > xins, gty = zins > yins, ltx = zins < xins, lty = zins < yins;
+        const bool edge = upper ? (ltx || lty) : (gtx || gty);
+        const bool xgt = xins > yins;
+        // extra vertex: lower edge (1,-1) / (-1,1), lower interior (1,1);
+        // upper edge (2,0) / (0,2), upper interior (0,0)
+        const int ea = edge ? (upper ? (xgt ? 2 : 0) : (xgt ? 1 : -1)) : (upper ? 0 : 1);
+        const int eb = edge ? (upper ? (xgt ? 0 : 2) : (xgt ? -1 : 1)) : (upper ? 0 : 1);
+        const float fea = edge ? (upper ? (xgt ? 2.f : 0.f) : (xgt ? 1.f : -1.f)) : (upper ? 0.f : 1.f);
+        const float feb = edge ? (upper ? (xgt ? 0.f : 2.f) : (xgt ? -1.f : 1.f)) : (upper ? 0.f : 1.f);
+        const int c = upper ? 1 : 0;
+        const float fc = upper ? 1.f : 0.f;
+        const float xf = static_cast<float>(xins), yf = static_cast<float>(yins);
+        const float sf = (xf + yf) * S;
+        const float dx0 = xf + sf, dy0 = yf + sf;
+        float nv;
+        if (kTable) {
+            const TableRow g{tab + exact_int32(yb - by) * nx + exact_int32(xb - bx), nx};
+            nv = contrib(g, gv, 1, 0, 1.0f, 0.0f, dx0, dy0);
+            nv += contrib(g, gv, 0, 1, 0.0f, 1.0f, dx0, dy0);
+            nv += contrib(g, gv, c, c, fc, fc, dx0, dy0);
+            nv += contrib(g, gv, ea, eb, fea, feb, dx0, dy0);
+        } else {
+            const HashVtx g{base, __double2ll_rd(xb), __double2ll_rd(yb)};
+            nv = contrib(g, gv, 1, 0, 1.0f, 0.0f, dx0, dy0);
+            nv += contrib(g, gv, 0, 1, 0.0f, 1.0f, dx0, dy0);
+            nv += contrib(g, gv, c, c, fc, fc, dx0, dy0);
+            nv += contrib(g, gv, ea, eb, fea, feb, dx0, dy0);
+        }
+        acc[j] = fmaf(amp, nv * (1.0f / 47.0f), acc[j]);
+    }
+}
 
 __global__ void __launch_bounds__(kThreads)
 simplex2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
@@ -151,8 +164,8 @@ simplex2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) 
     __shared__ float2 gv[8];  // (+-5, +-2) / (+-2, +-5): bit 0 swaps, bits 1 / 2 negate x / y
     if (threadIdx.x < 8) {
         const int i = threadIdx.x;
-        const float gx = (i & 1) ? 2.0f : 5.0f, gy = (i & 1) ? 5.0f : 2.0f;
-        gv[i] = make_float2((i & 2) ? -gx : gx, (i & 4) ? -gy : gy);
+        const float gxv = (i & 1) ? 2.0f : 5.0f, gyv = (i & 1) ? 5.0f : 2.0f;
+        gv[i] = make_float2((i & 2) ? -gxv : gxv, (i & 4) ? -gyv : gyv);
     }
     __syncthreads();
     for (int o = 0; o < args.octaves; ++o) {
@@ -167,34 +180,34 @@ simplex2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) 
     }
     __syncthreads();
     const int c0 = lane * 4, r0 = warp * 8;
+    double gx[4];  // pixel centres g + 0.5 (exact)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gx[j] = static_cast<double>(tx0 + c0 + j) + 0.5;
     const int64_t lx0 = tx0 + c0 - args.ox;
-    const int64_t ly0 = ty0 + r0 - args.oy;
     float* out_map = out + static_cast<int64_t>(blockIdx.z) * args.map_stride;
-    // one pixel at a time, octaves innermost (the evaluation has data-dependent
-    // branches; a register array indexed by a rolled loop would spill)
 #pragma unroll 1
-    for (int p = 0; p < 32; ++p) {
-        const int r = p >> 2, j = p & 3;
-        const double gx = static_cast<double>(tx0 + c0 + j), gy = static_cast<double>(ty0 + r0 + r);
-        float acc = 0.f;
+    for (int r = 0; r < 8; ++r) {
+        const double gy = static_cast<double>(ty0 + r0 + r) + 0.5;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
         for (int o = 0; o < args.octaves; ++o) {
             const OctDev& od = args.oct[o];
-            const double fr = od.ratio;  // freq / R, IEEE division on the host
-            const double u = __dmul_rn(__dadd_rn(gx, 0.5), fr);
-            const double v = __dmul_rn(__dadd_rn(gy, 0.5), fr);
-            const double so = (u + v) * kStretch;
-            const double xs = u + so, ys = v + so;
-            const double xb = floor(xs), yb = floor(ys);
-            float nv;
             if (od.mode)
-                nv = opensimplex(TableGrad(gtab + od.goff, od.ncx, plan[o].bx, plan[o].by, xb, yb), gv, u, v, xb,
-                                 yb, xs, ys);
+                os_octave4<true>(acc, gv, od.ratio, od.amp, gtab + od.goff, od.ncx, plan[o].bx, plan[o].by, 0, gx, gy);
             else
-                nv = opensimplex(HashGrad(seed_key + od.oct_key, xb, yb), gv, u, v, xb, yb, xs, ys);
-            acc = fmaf(od.amp, nv, acc);
+                os_octave4<false>(acc, gv, od.ratio, od.amp, nullptr, 0, 0.0, 0.0, seed_key + od.oct_key, gx, gy);
         }
-        const int64_t ly = ly0 + r, lx = lx0 + j;
-        if (ly >= 0 && ly < args.height && lx >= 0 && lx < args.width) out_map[ly * args.ld + lx] = acc;
+        const int64_t ly = ty0 + r0 + r - args.oy;
+        if (ly >= 0 && ly < args.height) {
+            float* row = out_map + ly * args.ld;
+            if (lx0 >= 0 && lx0 + 4 <= args.width && ((reinterpret_cast<uintptr_t>(row + lx0) & 15) == 0)) {
+                *reinterpret_cast<float4*>(row + lx0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (lx0 + j >= 0 && lx0 + j < args.width) row[lx0 + j] = acc[j];
+            }
+        }
     }
 }
 
