@@ -42,21 +42,30 @@ def main():
         bufs[i % 3].fill_(1.0)
     e1.record()
     torch.cuda.synchronize()
-    wpeak = 4 * R * R / (e0.elapsed_time(e1) / 200 * 1e-3) / 1e9
+    wpeak = 4 * R * R / (e0.elapsed_time(e1) / 200 * 1e-3) / 1e9  # (fill_ launches stay ahead of the GPU)
     rows = []
     for n in range(1, 17):
         cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=R, base_frequency=8,
                            octaves=n)
         for i in range(5):
             pt.generate_into_device(cfg, (0, 0), R, bufs[i % 3])
+        # device rate: the launches replayed from a CUDA graph (a Python loop of
+        # C-ABI calls issues one launch per ~18 us, slower than the few-octave
+        # kernels themselves)
+        st = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(args.iters):
+                pt.generate_into_device(cfg, (0, 0), R, bufs[i % 3], stream=st)
+        g.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
-        for i in range(args.iters):
-            pt.generate_into_device(cfg, (0, 0), R, bufs[i % 3])
+        for _ in range(3):
+            g.replay()
         e1.record()
         torch.cuda.synchronize()
-        s = e0.elapsed_time(e1) / args.iters * 1e-3
+        s = e0.elapsed_time(e1) / (3 * args.iters) * 1e-3
         so = R * R * n / s
         tf = 7 * so / 1e12
         gbs = 4 * R * R / s / 1e9
@@ -68,7 +77,7 @@ def main():
               f"{gbs:7.1f} GB/s ({gbs/hbm:5.1%})", flush=True)
     res = {"workload": "4096^2 zg_paper S5, f0 = 8, ratio 2, persistence 0.5", "ffma_peak_tflops": peak,
            "hbm_peak_gbs": hbm, "write_fill_gbs": wpeak,
-           "note": "hbm_frac against MEASURED_PEAKS.json hbm_gbs; write_frac_vs_fill against a torch fill_ of the "
+           "note": "device time per launch from CUDA-graph replays of `iters` launches (3 rotating 64 MiB outputs); hbm_frac against MEASURED_PEAKS.json hbm_gbs; write_frac_vs_fill against a torch fill_ of the "
                    "same 64 MiB buffers measured in this run (write-only ceiling)", "rows": rows}
     if args.out:
         with open(args.out, "w") as f:
