@@ -147,11 +147,14 @@ def cfg5_terrain(lib, world: int, rank: int, steps: int = 3, analysis: bool = Tr
     ccfg = cfg.to_c()
     sizes, lags = [2, 4, 8, 16, 32, 64], [1 << i for i in range(13)]
     band = plan_band(T5, T5, world, rank, align=1024, max_lag=max(lags))
-    out = torch.empty((band.rows, T5), dtype=torch.float32, device=dev)
+    # the band buffer of the analysis: halo row, owned rows, lookahead rows; the
+    # generation step writes the owned rows in place (row offset halo_top)
+    buf = torch.empty((band.gen_rows, T5), dtype=torch.float32, device=dev)
+    own = buf.data_ptr() + 4 * band.halo_top * T5
     stream = torch.cuda.current_stream(dev).cuda_stream
 
     def gen():
-        assert lib.tg_fbm_generate_rect_f32(C.byref(ccfg), 0, band.y0, T5, band.rows, out.data_ptr(), T5,
+        assert lib.tg_fbm_generate_rect_f32(C.byref(ccfg), 0, band.y0, T5, band.rows, own, T5,
                                             stream) == 0, _abi.last_error()
 
     gen()
@@ -168,15 +171,14 @@ def cfg5_terrain(lib, world: int, rank: int, steps: int = 3, analysis: bool = Tr
     if world > 1:
         torch.distributed.all_reduce(g, op=torch.distributed.ReduceOp.MAX)
     gen_ms = float(g.item())
-    del out
     res = {"workload": f"config 5: {T5}^2 zg_paper S5, {OCT5} octaves, base cell 1024 px, {world} row band(s)",
            "gen_ms": gen_ms, "sample_octaves_per_s": float(T5) * T5 * OCT5 / (gen_ms * 1e-3),
            "band_rows": band.rows, "scaling": "strong (fixed 32768^2 terrain)"}
     if not analysis:
         return res
     comm = Comm.nccl(device=dev)
-    be = DeviceBackend(cfg, device=dev)
-    terrain_stats(band, be, comm, sizes, lags)  # warm-up (module loading, band buffer)
+    be = DeviceBackend(cfg, device=dev, buffer=buf, owned_ready=True)
+    terrain_stats(band, be, comm, sizes, lags)  # warm-up (module loading, selection buffers)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -188,11 +190,12 @@ def cfg5_terrain(lib, world: int, rank: int, steps: int = 3, analysis: bool = Tr
         torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
     comm.close()
     res.update({"analysis_ms": float(a.item()) * 1e3,
-                "analysis_note": "tg_terrain_stats_band per rank (band + halo/lookahead regenerated, median, "
-                                 "coastline + box count, variogram 13 lags x 2 axes), statistics all-reduced "
-                                 "by NCCL; host wall clock, max over ranks",
+                "analysis_note": "tg_terrain_stats_band_buf per rank on the generated band (halo / lookahead rows "
+                                 "regenerated, none at N=1; upper median, coastline + box count, variogram 13 lags "
+                                 "x 2 axes), statistics all-reduced by NCCL; host wall clock, max over ranks",
                 "sea_level": st.sea_level, "land_fraction": st.land_fraction, "box_counts": st.counts,
                 "d_box": st.d_box, "hurst": st.hurst, "d_variogram": st.d_variogram})
+    del buf
     return res
 
 

@@ -342,6 +342,19 @@ int tg_terrain_stats_band(const tg_fbm_config* cfg, const tg_terrain* t, const t
                           int32_t n_lags, const double* sea_level, tg_comm* comm,
                           tg_terrain_stats* out, void* stream);
 
+/* The same product path over a band buffer the caller owns: dev_band_buf
+ * holds (halo_top + rows + below) rows of width floats (pitch = width), its
+ * first row being global row y0 - halo_top.  owned_ready != 0: the caller has
+ * already generated the owned rows into it (at row offset halo_top, e.g. with
+ * tg_fbm_generate_rect_f32 — the terrain's own generation step), and only the
+ * halo row above and the lookahead rows below are regenerated here (a single
+ * band regenerates nothing).  owned_ready == 0: every row is generated here. */
+int tg_terrain_stats_band_buf(const tg_fbm_config* cfg, const tg_terrain* t, const tg_band* band,
+                              float* dev_band_buf, int32_t owned_ready, const int32_t* sizes,
+                              int32_t n_sizes, const int32_t* lags, int32_t n_lags,
+                              const double* sea_level, tg_comm* comm, tg_terrain_stats* out,
+                              void* stream);
+
 /* The same driver over caller-supplied band operations — the test hook of the
  * host logic (the reference's Source policy plays this role for generation,
  * fbm.hpp:110-133).  The product path above never uses it. */

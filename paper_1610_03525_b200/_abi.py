@@ -165,6 +165,8 @@ SIGNATURES = {
     "tg_plan_band": (C.c_int, [C.POINTER(TgTerrain), I32, I32, C.POINTER(TgBand)]),
     "tg_terrain_stats_band": (C.c_int, [PCFG, C.POINTER(TgTerrain), C.POINTER(TgBand), P, I32, P, I32,
                                         C.POINTER(F64), P, C.POINTER(TgTerrainStats), P]),
+    "tg_terrain_stats_band_buf": (C.c_int, [PCFG, C.POINTER(TgTerrain), C.POINTER(TgBand), P, I32, P, I32, P,
+                                            I32, C.POINTER(F64), P, C.POINTER(TgTerrainStats), P]),
     "tg_terrain_stats_ops": (C.c_int, [C.POINTER(TgTerrain), C.POINTER(TgBand), P, I32, P, I32, C.POINTER(F64), P,
                                        C.POINTER(TgBandOps), C.POINTER(TgTerrainStats)]),
 }

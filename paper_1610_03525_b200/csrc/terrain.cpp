@@ -139,6 +139,8 @@ struct DeviceBand {
     float* buf = nullptr;  // gen rows x width, contiguous
     cudaStream_t st;
     tg::SelectCache sel;   // candidate keys kept by the first median pass
+    float* ext = nullptr;  // caller's band buffer (tg_terrain_stats_band_buf)
+    bool owned_ready = false;  // ... whose owned rows the caller already generated
 
     const float* owned() const { return buf + b->halo_top * t->width; }
     bool last() const { return b->y0 - t->y_origin + b->rows >= t->height; }
@@ -174,6 +176,22 @@ float* band_buffer(size_t bytes, int* err) {
 int dev_generate(void* ctx, const tg_band* b) {
     auto* d = static_cast<DeviceBand*>(ctx);
     const int64_t gen_rows = b->halo_top + b->rows + b->below;
+    const int64_t W = d->t->width;
+    if (d->ext && d->owned_ready) {  // regenerate only the halo row above and the lookahead rows below
+        d->buf = d->ext;
+        if (b->halo_top)
+            if (int st = tg_fbm_generate_rect_f32(d->cfg, d->t->x0, b->y0 - b->halo_top, W, b->halo_top, d->buf, W,
+                                                  d->st))
+                return st;
+        if (b->below)
+            return tg_fbm_generate_rect_f32(d->cfg, d->t->x0, b->y0 + b->rows, W, b->below,
+                                            d->buf + (b->halo_top + b->rows) * W, W, d->st);
+        return TG_OK;
+    }
+    if (d->ext) {
+        d->buf = d->ext;
+        return tg_fbm_generate_rect_f32(d->cfg, d->t->x0, b->y0 - b->halo_top, W, gen_rows, d->buf, W, d->st);
+    }
     int err = TG_OK;
     d->buf = band_buffer(static_cast<size_t>(gen_rows) * static_cast<size_t>(d->t->width) * sizeof(float), &err);
     if (!d->buf) return err;
@@ -438,6 +456,22 @@ int tg_terrain_stats_band(const tg_fbm_config* cfg, const tg_terrain* t, const t
     // one band: the local median is the global one (narrow candidate window);
     // several: the global median's local rank is unknown (wide window)
     d.sel.delta = comm && comm->nranks > 1 ? 0.05 : 0.005;
+    tg_band_ops ops{&d, dev_generate, dev_histogram, dev_boxcount, dev_variogram};
+    const int st = tg_terrain_stats_ops(t, b, sizes, n_sizes, lags, n_lags, sea_level, comm, &ops, out);
+    tg::select_cache_free(&d.sel, d.st);
+    return st;
+}
+
+int tg_terrain_stats_band_buf(const tg_fbm_config* cfg, const tg_terrain* t, const tg_band* b, float* dev_band_buf,
+                              int32_t owned_ready, const int32_t* sizes, int32_t n_sizes, const int32_t* lags,
+                              int32_t n_lags, const double* sea_level, tg_comm* comm, tg_terrain_stats* out,
+                              void* stream) {
+    if (!cfg || !t || !b || !dev_band_buf) return tg::set_error(TG_EVALIDATION, "terrain_stats: null argument");
+    if (int st = tg::check_device()) return st;
+    DeviceBand d{cfg, t, b, nullptr, static_cast<cudaStream_t>(stream)};
+    d.sel.delta = comm && comm->nranks > 1 ? 0.05 : 0.005;
+    d.ext = dev_band_buf;
+    d.owned_ready = owned_ready != 0;
     tg_band_ops ops{&d, dev_generate, dev_histogram, dev_boxcount, dev_variogram};
     const int st = tg_terrain_stats_ops(t, b, sizes, n_sizes, lags, n_lags, sea_level, comm, &ops, out);
     tg::select_cache_free(&d.sel, d.st);

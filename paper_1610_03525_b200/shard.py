@@ -210,7 +210,14 @@ def terrain_stats(band: Band, backend, comm: Comm, sizes: Sequence[int], lags: S
     lg = (C.c_int32 * len(lags))(*lags)
     sea = C.byref(C.c_double(sea_level)) if sea_level is not None else None
     st = _abi.TgTerrainStats()
-    if isinstance(backend, DeviceBackend):
+    if isinstance(backend, DeviceBackend) and backend.buffer is not None:
+        buf = backend.buffer
+        if buf.numel() < band.gen_rows * band.width or not buf.is_contiguous() or buf.device.type != "cuda":
+            raise ValueError("terrain_stats: band buffer must be a contiguous CUDA tensor of gen_rows x width")
+        _check(lib.tg_terrain_stats_band_buf(C.byref(backend.ccfg), C.byref(t), C.byref(b), buf.data_ptr(),
+                                             1 if backend.owned_ready else 0, sz, len(sizes), lg, len(lags), sea,
+                                             comm.handle, C.byref(st), backend._sp()))
+    elif isinstance(backend, DeviceBackend):
         _check(lib.tg_terrain_stats_band(C.byref(backend.ccfg), C.byref(t), C.byref(b), sz, len(sizes), lg,
                                          len(lags), sea, comm.handle, C.byref(st), backend._sp()))
     else:
@@ -274,15 +281,20 @@ def distributed_upper_median(hist_fn, total: int, comm: Comm) -> float:
 
 class DeviceBackend:
     """The product backend: the band generated and analysed on this rank's GPU
-    inside tg_terrain_stats_band."""
+    inside tg_terrain_stats_band — or, with `buffer` (a float32 CUDA tensor of
+    gen_rows x width whose owned rows the caller has generated when
+    `owned_ready`), tg_terrain_stats_band_buf, which regenerates only the halo
+    and lookahead rows."""
 
-    def __init__(self, cfg: FbmConfig, device=None, stream=None):
+    def __init__(self, cfg: FbmConfig, device=None, stream=None, buffer=None, owned_ready: bool = False):
         import torch
 
         self.cfg = cfg
         self.ccfg = cfg.to_c()
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.stream = stream
+        self.buffer = buffer
+        self.owned_ready = owned_ready
 
     def _sp(self) -> int:
         import torch
