@@ -472,8 +472,10 @@ int vg_ring_enqueue(const float* z, int64_t W, int64_t H, int64_t ld, int64_t P,
         if (items[kd] == 0) continue;
         const int64_t grid =
             std::max<int64_t>(1, std::min<int64_t>((items[kd] + kWarps - 1) / kWarps, per_sm * static_cast<int64_t>(sm)));
-        kt[all ? 1 : 0][kd]<<<static_cast<unsigned>(grid), kThreads, smem, kd < 3 ? s : sy>>>(z, W, ld, P, vec, plan, wp,
-                                                                                              sums);
+        // the HBM-bound class-2 walks (kinds 2, 5) on the side stream beside the
+        // fp64-bound classes 0 / 1 when the caller forked one (TG_VG_CONCURRENT)
+        kt[all ? 1 : 0][kd]<<<static_cast<unsigned>(grid), kThreads, smem, (kd == 2 || kd == 5) ? sy : s>>>(
+            z, W, ld, P, vec, plan, wp, sums);
         if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "variogram walks");
     }
     return 0;
