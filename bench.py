@@ -46,6 +46,46 @@ FLOPS_PER_SAMPLE_OCTAVE = 7  # zg: paper's 3 mul + 3 add + 1 accu
 BYTES_PER_SAMPLE = 4         # one fp32 store per sample, no inputs
 
 
+# TG_BENCH_SHARED_GPU=1: a logic smoke test of the N-rank code paths on a
+# one-GPU box — every rank on cuda:0, gloo for the process group and a host
+# all-reduce hook for the statistics instead of NCCL (no rank's kernels wait on
+# another's).  Not a measurement: the ranks share one GPU.
+SHARED_GPU = os.environ.get("TG_BENCH_SHARED_GPU", "0") == "1"
+
+
+def _device_index(local: int) -> int:
+    return 0 if SHARED_GPU else local
+
+
+def _init_dist(local: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    if SHARED_GPU:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+def _max_over_ranks(t):
+    """All-reduce MAX of a one-element tensor (on the device under NCCL)."""
+    import torch.distributed as dist
+
+    if SHARED_GPU:
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        t.copy_(c)
+    else:
+        _max_over_ranks(t)
+    return t
+
+
+def _stats_comm(device):
+    from paper_1610_03525_b200.shard import Comm
+
+    return Comm() if SHARED_GPU else Comm.nccl(device=device)
+
+
 def workload_cfg(world: int, rank: int):
     import paper_1610_03525_b200 as pt
 
@@ -79,7 +119,7 @@ def analysis_pass(lib, ccfg, buf, stream_ptr, world, rank):
     from paper_1610_03525_b200 import _abi
     from paper_1610_03525_b200.shard import Comm, distributed_upper_median
 
-    comm = Comm.nccl(device=torch.device("cuda", torch.cuda.current_device()))
+    comm = _stats_comm(torch.device("cuda", torch.cuda.current_device()))
     sizes = [2, 4, 8, 16, 32, 64]
     lags = [1 << i for i in range(12)]
 
@@ -169,14 +209,14 @@ def cfg5_terrain(lib, world: int, rank: int, steps: int = 3, analysis: bool = Tr
     torch.cuda.synchronize()
     g = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
     if world > 1:
-        torch.distributed.all_reduce(g, op=torch.distributed.ReduceOp.MAX)
+        _max_over_ranks(g)
     gen_ms = float(g.item())
     res = {"workload": f"config 5: {T5}^2 zg_paper S5, {OCT5} octaves, base cell 1024 px, {world} row band(s)",
            "gen_ms": gen_ms, "sample_octaves_per_s": float(T5) * T5 * OCT5 / (gen_ms * 1e-3),
            "band_rows": band.rows, "scaling": "strong (fixed 32768^2 terrain)"}
     if not analysis:
         return res
-    comm = Comm.nccl(device=dev)
+    comm = _stats_comm(dev)
     be = DeviceBackend(cfg, device=dev, buffer=buf, owned_ready=True)
     terrain_stats(band, be, comm, sizes, lags)  # warm-up (module loading, selection buffers)
     torch.cuda.synchronize()
@@ -187,7 +227,7 @@ def cfg5_terrain(lib, world: int, rank: int, steps: int = 3, analysis: bool = Tr
     torch.cuda.synchronize()
     a = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if world > 1:
-        torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
+        _max_over_ranks(a)
     comm.close()
     res.update({"analysis_ms": float(a.item()) * 1e3,
                 "analysis_note": "tg_terrain_stats_band_buf per rank on the generated band (halo / lookahead rows "
@@ -397,9 +437,10 @@ def run_cfg5_workload(args, rank: int, world: int, local: int) -> None:
     from paper_1610_03525_b200 import _abi
     from paper_1610_03525_b200.shard import plan_band
 
+    local = _device_index(local)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        _init_dist(local)
     lib = _abi.load()
     cfg = pt.FbmConfig(seed=1, method=pt.Method.zg_paper, smoothstep=5, resolution=T5, base_frequency=F05,
                        octaves=OCT5)
@@ -432,7 +473,7 @@ def run_cfg5_workload(args, rank: int, world: int, local: int) -> None:
         torch.cuda.synchronize()
     t = torch.tensor([ev[0].elapsed_time(ev[1])], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _max_over_ranks(t)
     total_ms = float(t.item())
     so_step = float(T5) * T5 * OCT5
     value = so_step * K / (total_ms * 1e-3)
@@ -455,7 +496,7 @@ def run_cfg5_workload(args, rank: int, world: int, local: int) -> None:
             assert lib.tg_fbm_generate_f64_host(C.byref(ccfg), x, y, C4, host.data_ptr(), C4 * C4) == 0
     te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        _max_over_ranks(te)
     e2e_value = so_step * e2e_steps / float(te.item())
     stats = cfg5_terrain(lib, world, rank, steps=1, analysis=not args.no_analysis)
     if rank == 0:
@@ -515,9 +556,10 @@ def main() -> None:
     import paper_1610_03525_b200 as pt
     from paper_1610_03525_b200 import _abi
 
+    local = _device_index(local)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        _init_dist(local)
     lib = _abi.load()
     cfg, origin = workload_cfg(world, rank)
     ccfg = cfg.to_c()
@@ -574,7 +616,7 @@ def main() -> None:
     isolated_us = statistics.median(iso) * 1e3
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _max_over_ranks(t)
     total_ms_max = float(t.item())
 
     so_per_step = float(R * R * OCTAVES)
@@ -601,7 +643,7 @@ def main() -> None:
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        _max_over_ranks(te)
     e2e_value = so_per_step * e2e_steps * world / float(te.item())
     # the reference's callers pass a std::vector<double> (pageable): same call
     # into a pageable buffer, reported beside the pinned headline
