@@ -91,7 +91,10 @@ __device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) { return a >= 0 ? 
 // registers.  Layout per stage: [seq][step][lane] floats (each lane reads back
 // only what it copied: no warp synchronisation), or for the contiguous X0 walk
 // [lane][R + 4] (16-byte copies, conflict-free 16-byte reads).
-constexpr int kStages = 3;
+#ifndef TG_VGR_STAGES
+#define TG_VGR_STAGES 4
+#endif
+constexpr int kStages = TG_VGR_STAGES;  // chunks staged per warp (kStages - 1 in flight)
 constexpr int kStageFloats = 32 * 20;  // >= NS * R * 32 and 32 * (16 + 4)
 __device__ __forceinline__ void cp_async4z(uint32_t dst, const float* src, bool ok) {  // zero-filled if !ok
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
@@ -235,15 +238,14 @@ __device__ __forceinline__ void walk(float* stage, const float* const (&b)[NS], 
         }
     };
     auto step = [&](int q, const double (&prev)[NS][R], double (&cur)[NS][R]) {
-        cp_wait<1>();  // chunk q has landed (q + 1 may still be in flight)
+        cp_wait<kStages - 2>();  // chunk q has landed (q + 1 .. may still be in flight)
         chunk(q, prev, cur);
-        issue(q + 2);  // into the slot of chunk q - 1 (read by chunk q's edge path)
+        issue(q + kStages - 1);  // into the slot of chunk q - 1 (read by chunk q's edge path)
     };
     double ra[NS][R], rb[NS][R];
-    issue(-1);
-    issue(0);
-    issue(1);
-    cp_wait<2>();
+#pragma unroll
+    for (int q = -1; q < kStages - 1; ++q) issue(q);
+    cp_wait<kStages - 1>();
 #pragma unroll
     for (int i = 0; i < NS; ++i)
 #pragma unroll
