@@ -87,6 +87,21 @@ def test_no_cpu_fallback(lib):
     assert "no CPU fallback" in lib.tg_last_error().decode()
 
 
+def test_terrain_stats_buffer_validation(lib):
+    """tg_terrain_stats_band_buf rejects a null band buffer before touching a device."""
+    from paper_1610_03525_b200 import _abi
+
+    c = make_cfg()
+    t = _abi.TgTerrain(0, 64, 0, 64, 64, 1)
+    b = _abi.TgBand(0, 64, 0, 0)
+    sz = (C.c_int32 * 3)(2, 4, 8)
+    lg = (C.c_int32 * 1)(1)
+    st = _abi.TgTerrainStats()
+    assert lib.tg_terrain_stats_band_buf(C.byref(c), C.byref(t), C.byref(b), None, 1, sz, 3, lg, 1, None, None,
+                                         C.byref(st), None) == 1
+    assert "null argument" in lib.tg_last_error().decode()
+
+
 def test_python_mirror_surface():
     import paper_1610_03525_b200 as pt
 
