@@ -7,8 +7,8 @@
 // TG_METHOD_PERLIN_PERM.
 //
 // Per CTA (128 x 64 tile, 256 threads, 4 x 8 pixels per thread) the seed's
-// table is built in shared memory: thread i hashes key_i and ranks it among
-// the 256 keys (a sort by key, so no sequential shuffle), then P and the
+// table is built in shared memory: thread i hashes key_i, and a bitonic sort
+// of the (key, index) pairs gives the permutation (no sequential shuffle), then P and the
 // gradient of every table entry (the 8 unit vectors at k * 45 degrees) are
 // laid out twice (512 entries) so that P[a + iy] needs no wrap.  Octaves run
 // outermost: cell index and position per column / row (the fast path's
@@ -73,15 +73,28 @@ __global__ void __launch_bounds__(kThreads) perm2d_kernel(const __grid_constant_
     }
     __syncthreads();
     {
-        const uint64_t k = key[tid];
-        int rank = 0;
-#pragma unroll 8
-        for (int j = 0; j < 256; ++j) {
-            const uint64_t kj = key[j];
-            rank += kj < k || (kj == k && j < tid);
+        // the permutation = the indices sorted by (key, index): a bitonic sort
+        // in shared memory (36 compare-exchange steps; ranking every key
+        // against all 256 cost ~1.5 k instructions per thread and CTA)
+        __shared__ uint8_t idx[256];
+        idx[tid] = static_cast<uint8_t>(tid);
+        __syncthreads();
+        for (int k = 2; k <= 256; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const int p = tid ^ j;
+                if (p > tid) {
+                    const uint64_t ka = key[tid], kb = key[p];
+                    const uint8_t ia = idx[tid], ib = idx[p];
+                    const bool gt = ka > kb || (ka == kb && ia > ib);
+                    if (gt == ((tid & k) == 0)) {
+                        key[tid] = kb, key[p] = ka;
+                        idx[tid] = ib, idx[p] = ia;
+                    }
+                }
+                __syncthreads();
+            }
         }
-        P2[rank] = static_cast<uint8_t>(tid);
-        P2[rank + 256] = static_cast<uint8_t>(tid);
+        P2[tid] = P2[tid + 256] = idx[tid];
     }
     __syncthreads();
     {

@@ -24,6 +24,8 @@ CONFIGS = {
     "cfg3g": (dict(seed=1, method=pt.Method.generic, resolution=4096, base_frequency=8, octaves=12), 4096, 4096),
     "cfg3s": (dict(seed=1, method=pt.Method.opensimplex, resolution=4096, base_frequency=8, octaves=12), 4096,
               4096),
+    "cfg3pp": (dict(seed=1, method=pt.Method.perlin_perm, resolution=4096, base_frequency=8, octaves=12), 4096,
+               4096),
     "cfg5": (dict(seed=1, smoothstep=5, resolution=32768, base_frequency=32, octaves=16), 4096, 4096),
 }
 
