@@ -57,8 +57,65 @@ __device__ __forceinline__ void cell_coord(const OctDev& od, double R, int64_t g
     }
 }
 
+// ppc = 1 << SH in {1, 2}: the thread's 4 x 8 pixels cover NCX x NCY cells;
+// the corner rows are swept top to bottom keeping the previous row's
+// gradients, so each corner gradient is read once ((NCX + 1) x (NCY + 1)
+// reads instead of 4 per pixel), and each cell factorises as in the ppc >= 4
+// path.
+template <int SH, int ORDER>
+__device__ __forceinline__ void perm_small(float (&acc)[8][4], const OctDev& od, const uint8_t* P2, const float2* GP,
+                                           int64_t gx0, int64_t gy0, int ox, int oy, float amp) {
+    constexpr int NCX = 4 >> SH, NCY = 8 >> SH, CPC = 1 << SH, RPC = 1 << SH;
+    const int64_t ix0 = gx0 >> SH, iy0 = gy0 >> SH;
+    int a[NCX + 1];
+#pragma unroll
+    for (int i = 0; i <= NCX; ++i) a[i] = P2[static_cast<int>((ix0 + i + ox) & 255)];
+    float x[4], sx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        x[j] = (static_cast<float>((gx0 + j) & (CPC - 1)) + 0.5f) * od.inv_ppc;
+        sx[j] = fade<ORDER>(x[j]);
+    }
+    float2 top[NCX + 1];
+    const int iyo0 = static_cast<int>((iy0 + oy) & 255);
+#pragma unroll
+    for (int i = 0; i <= NCX; ++i) top[i] = GP[a[i] + iyo0];
+#pragma unroll
+    for (int cy = 0; cy < NCY; ++cy) {
+        const int iyo = static_cast<int>((iy0 + cy + 1 + oy) & 255);
+        float2 bot[NCX + 1];
+#pragma unroll
+        for (int i = 0; i <= NCX; ++i) bot[i] = GP[a[i] + iyo];
+#pragma unroll
+        for (int cx = 0; cx < NCX; ++cx) {
+            const float2 g00 = top[cx], g10 = top[cx + 1], g01 = bot[cx], g11 = bot[cx + 1];
+#pragma unroll
+            for (int jj = 0; jj < CPC; ++jj) {
+                const int j = cx * CPC + jj;
+                const float a0 = g00.x * x[j], a1 = g10.x * (x[j] - 1.f);
+                const float b0 = g01.x * x[j], b1 = g11.x * (x[j] - 1.f);
+                const float P0 = fmaf(sx[j], a1 - a0, a0), Q0 = fmaf(sx[j], g10.y - g00.y, g00.y);
+                const float P1 = fmaf(sx[j], b1 - b0, b0), Q1 = fmaf(sx[j], g11.y - g01.y, g01.y);
+#pragma unroll
+                for (int rr = 0; rr < RPC; ++rr) {
+                    const int r = cy * RPC + rr;
+                    const float y = (static_cast<float>(rr) + 0.5f) * od.inv_ppc;
+                    const float sy = fade<ORDER>(y), ym = y - 1.f;
+                    const float h0 = fmaf(y, Q0, P0), h1 = fmaf(ym, Q1, P1);
+                    acc[r][j] = fmaf(amp, fmaf(sy, h1 - h0, h0), acc[r][j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i <= NCX; ++i) top[i] = bot[i];
+    }
+}
+
+#ifndef TG_PERM_MINB
+#define TG_PERM_MINB 2
+#endif
 template <int ORDER>
-__global__ void __launch_bounds__(kThreads) perm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
+__global__ void __launch_bounds__(kThreads, TG_PERM_MINB) perm2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) {
     __shared__ uint64_t key[256];
     __shared__ uint8_t P2[512];
     __shared__ float2 GP[512];
@@ -98,10 +155,14 @@ __global__ void __launch_bounds__(kThreads) perm2d_kernel(const __grid_constant_
     }
     __syncthreads();
     {
+        // the 8 unit gradients at k * 45 degrees, selected without a local array
         constexpr float R = 0.70710678118654752f;
-        const float2 G[8] = {{1.f, 0.f}, {R, R}, {0.f, 1.f}, {-R, R}, {-1.f, 0.f}, {-R, -R}, {0.f, -1.f}, {R, -R}};
         const int k = P2[tid] & 7;
-        GP[tid] = GP[tid + 256] = G[k];
+        const float c = (k & 1) ? R : 1.f, z = (k & 1) ? R : 0.f;  // |component| on / off the axis
+        const int q = k >> 1;                                         // quadrant
+        const float gx = q == 0 ? c : q == 1 ? -z : q == 2 ? -c : z;
+        const float gy = q == 0 ? z : q == 1 ? c : q == 2 ? -z : -c;
+        GP[tid] = GP[tid + 256] = make_float2(gx, gy);
     }
     __syncthreads();
 
@@ -117,6 +178,59 @@ __global__ void __launch_bounds__(kThreads) perm2d_kernel(const __grid_constant_
         const OctDev& od = args.oct[o];
         if (od.cls == kClsSubInt || od.amp == 0.f) continue;  // lattice points: exactly 0
         const int ox = off[o][0], oy = off[o][1];
+        const float amp = od.amp;
+        if (od.cls == kClsFast && od.shift >= 2) {
+            // ppc >= 4 (aligned): the thread's 4 columns share one cell and each
+            // 4-row half of its rows one cell row, so the 4 corner gradients are
+            // read once per cell row and the cell factorises into column terms
+            // (kernels2d.hpp:163-173 regrouped): h0 = P0(x) + y Q0(x),
+            // h1 = P1(x) + (y - 1) Q1(x), v = h0 + S(y) (h1 - h0).
+            const int64_t ix = (tx0 + c0) >> od.shift;
+            const int a = P2[static_cast<int>((ix + ox) & 255)], b = P2[static_cast<int>((ix + 1 + ox) & 255)];
+            float x[4], sx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t r = (tx0 + c0 + j) & (static_cast<int64_t>(od.ppc) - 1);
+                x[j] = (static_cast<float>(r) + 0.5f) * od.inv_ppc;
+                sx[j] = fade<ORDER>(x[j]);
+            }
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) {
+                const int64_t iy = (ty0 + r0 + 4 * hr) >> od.shift;
+                const int iyo = static_cast<int>((iy + oy) & 255);
+                const float2 g00 = GP[a + iyo], g10 = GP[b + iyo], g01 = GP[a + iyo + 1], g11 = GP[b + iyo + 1];
+                float P0[4], Q0[4], P1[4], Q1[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float a0 = g00.x * x[j], a1 = g10.x * (x[j] - 1.f);
+                    const float b0 = g01.x * x[j], b1 = g11.x * (x[j] - 1.f);
+                    P0[j] = fmaf(sx[j], a1 - a0, a0);
+                    Q0[j] = fmaf(sx[j], g10.y - g00.y, g00.y);
+                    P1[j] = fmaf(sx[j], b1 - b0, b0);
+                    Q1[j] = fmaf(sx[j], g11.y - g01.y, g01.y);
+                }
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const int r = 4 * hr + rr;
+                    const int64_t ry = (ty0 + r0 + r) & (static_cast<int64_t>(od.ppc) - 1);
+                    const float y = (static_cast<float>(ry) + 0.5f) * od.inv_ppc;
+                    const float sy = fade<ORDER>(y), ym = y - 1.f;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float h0 = fmaf(y, Q0[j], P0[j]), h1 = fmaf(ym, Q1[j], P1[j]);
+                        acc[r][j] = fmaf(amp, fmaf(sy, h1 - h0, h0), acc[r][j]);
+                    }
+                }
+            }
+            continue;
+        }
+        if (od.cls == kClsFast && od.shift >= 0) {  // ppc 1 or 2
+            if (od.shift == 1)
+                perm_small<1, ORDER>(acc, od, P2, GP, tx0 + c0, ty0 + r0, ox, oy, amp);
+            else
+                perm_small<0, ORDER>(acc, od, P2, GP, tx0 + c0, ty0 + r0, ox, oy, amp);
+            continue;
+        }
         int a[4], b[4];
         float x[4], sx[4];
 #pragma unroll
@@ -127,7 +241,6 @@ __global__ void __launch_bounds__(kThreads) perm2d_kernel(const __grid_constant_
             a[j] = P2[static_cast<int>((ix + ox) & 255)];
             b[j] = P2[static_cast<int>((ix + 1 + ox) & 255)];
         }
-        const float amp = od.amp;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             int64_t iy;
