@@ -42,32 +42,25 @@ __device__ __forceinline__ int exact_int32(double v) {
     return __double2loint(v + 6755399441055744.0);
 }
 
-// Gradient index of vertex (xsb + a, ysb + b): per-CTA table row / hash.
-struct TableRow {
-    const uint8_t* row0;
-    int nx;
-    __device__ __forceinline__ uint32_t operator()(int a, int b) const { return row0[b * nx + a]; }
-};
-struct HashVtx {
-    uint64_t base;
-    int64_t xb, yb;
-    __device__ __forceinline__ uint32_t operator()(int a, int b) const { return grad_index(base, xb + a, yb + b); }
-};
-
-// (2 - d^2)^4 (g . d) for the vertex at offset (a, b) from (xsb, ysb):
-// d = d0 - (a, b) - (a + b) * squish; the radial term clamps at zero, so the
-// gradient is always read (branch-free).  g from the 8-entry vector table.
-template <class G>
-__device__ __forceinline__ float contrib(const G& grad, const float2* gv, int a, int b, float fa, float fb,
-                                         float dx0, float dy0) {
-    constexpr float S = static_cast<float>(kSquish);
-    const float s = (fa + fb) * S;
-    const float dx = dx0 - fa - s, dy = dy0 - fb - s;
-    float attn = fmaxf(2.0f - dx * dx - dy * dy, 0.0f);
-    const float2 g = gv[grad(a, b)];
+// (2 - d^2)^4 (g . d) of one vertex, d = d0 - (a + (a + b) S, b + (a + b) S)
+// with the displacement offsets given and gi its gradient index (table or
+// hash); the radial term clamps at zero, so the gradient is always read.
+__device__ __forceinline__ float contrib_at(const float2* gv, uint32_t gi, float ox, float oy, float dx0, float dy0,
+                                            float v) {
+    const float dx = dx0 - ox, dy = dy0 - oy;
+    float attn = fmaxf(fmaf(-dy, dy, fmaf(-dx, dx, 2.0f)), 0.0f);
+    const float2 g = gv[gi];
     attn *= attn;
-    return attn * attn * fmaf(g.x, dx, g.y * dy);
+    return fmaf(attn * attn, fmaf(g.x, dx, g.y * dy), v);
 }
+
+// The six extra vertices of the region logic (OpenSimplex 2014): upper edge
+// (2,0) / (0,2), upper interior (0,0), lower edge (1,-1) / (-1,1), lower
+// interior (1,1) — displacement offsets and the integer offsets.
+struct ExtraCase {
+    float ox, oy;
+    int a, b;
+};
 
 constexpr int kTW = 128, kTH = 64, kThreads = 256;
 constexpr int kTableMargin = 6;           // vertices beyond the tile's stretched range
@@ -94,7 +87,7 @@ struct TabPlan {
 // picks the oracle's vertices; the offsets from the cell origin in fp32 via
 // dx0 = xins + in_sum * squish (the oracle's x - (xsb + (xsb + ysb) squish)).
 template <bool kTable>
-__device__ __forceinline__ void os_octave4(float (&acc)[4], const float2* gv, double fr, float amp,
+__device__ __forceinline__ void os_octave4(float (&acc)[4], const float2* gv, const ExtraCase* ext, double fr, float amp,
                                            const uint8_t* tab, int nx, double bx, double by, uint64_t base,
                                            const double (&gx)[4], double gy) {
     constexpr float S = static_cast<float>(kSquish);
@@ -109,35 +102,32 @@ __device__ __forceinline__ void os_octave4(float (&acc)[4], const float2* gv, do
         const double in_sum = xins + yins;
         const bool upper = in_sum > 1.0;
         const double zins = (upper ? 2.0 : 1.0) - in_sum;
-        // branch-free region: the four comparisons, then selects (a divergent
-        // branch per pixel cost both paths)
-        const bool gtx = zins > xins, gty = zins > yins, ltx = zins < xins, lty = zins < yins;
-        const bool edge = upper ? (ltx || lty) : (gtx || gty);
+        // branch-free region: the four comparisons, then one case index (a
+        // divergent branch per pixel cost both paths; per-value selects ~23
+        // instructions): the extra vertex's offsets come from a shared table
+        const bool edge = upper ? (zins < xins || zins < yins) : (zins > xins || zins > yins);
         const bool xgt = xins > yins;
-        // extra vertex: lower edge (1,-1) / (-1,1), lower interior (1,1);
-        // upper edge (2,0) / (0,2), upper interior (0,0)
-        const int ea = edge ? (upper ? (xgt ? 2 : 0) : (xgt ? 1 : -1)) : (upper ? 0 : 1);
-        const int eb = edge ? (upper ? (xgt ? 0 : 2) : (xgt ? -1 : 1)) : (upper ? 0 : 1);
-        const float fea = edge ? (upper ? (xgt ? 2.f : 0.f) : (xgt ? 1.f : -1.f)) : (upper ? 0.f : 1.f);
-        const float feb = edge ? (upper ? (xgt ? 0.f : 2.f) : (xgt ? -1.f : 1.f)) : (upper ? 0.f : 1.f);
-        const int c = upper ? 1 : 0;
-        const float fc = upper ? 1.f : 0.f;
+        const int cs = (upper ? 0 : 3) + (edge ? (xgt ? 0 : 1) : 2);
+        const ExtraCase ec = ext[cs];
+        constexpr float C1 = 1.0f + 2.0f * S;
+        const float fc = upper ? C1 : 0.0f;  // (c, c) vertex displacement
         const float xf = static_cast<float>(xins), yf = static_cast<float>(yins);
         const float sf = (xf + yf) * S;
         const float dx0 = xf + sf, dy0 = yf + sf;
         float nv;
         if (kTable) {
-            const TableRow g{tab + exact_int32(yb - by) * nx + exact_int32(xb - bx), nx};
-            nv = contrib(g, gv, 1, 0, 1.0f, 0.0f, dx0, dy0);
-            nv += contrib(g, gv, 0, 1, 0.0f, 1.0f, dx0, dy0);
-            nv += contrib(g, gv, c, c, fc, fc, dx0, dy0);
-            nv += contrib(g, gv, ea, eb, fea, feb, dx0, dy0);
+            const uint8_t* r0 = tab + exact_int32(yb - by) * nx + exact_int32(xb - bx);
+            nv = contrib_at(gv, r0[1], 1.0f + S, S, dx0, dy0, 0.0f);
+            nv = contrib_at(gv, r0[nx], S, 1.0f + S, dx0, dy0, nv);
+            nv = contrib_at(gv, r0[upper ? nx + 1 : 0], fc, fc, dx0, dy0, nv);
+            nv = contrib_at(gv, r0[ec.b * nx + ec.a], ec.ox, ec.oy, dx0, dy0, nv);
         } else {
-            const HashVtx g{base, __double2ll_rd(xb), __double2ll_rd(yb)};
-            nv = contrib(g, gv, 1, 0, 1.0f, 0.0f, dx0, dy0);
-            nv += contrib(g, gv, 0, 1, 0.0f, 1.0f, dx0, dy0);
-            nv += contrib(g, gv, c, c, fc, fc, dx0, dy0);
-            nv += contrib(g, gv, ea, eb, fea, feb, dx0, dy0);
+            const int64_t xi = __double2ll_rd(xb), yi = __double2ll_rd(yb);
+            const int c = upper ? 1 : 0;
+            nv = contrib_at(gv, grad_index(base, xi + 1, yi), 1.0f + S, S, dx0, dy0, 0.0f);
+            nv = contrib_at(gv, grad_index(base, xi, yi + 1), S, 1.0f + S, dx0, dy0, nv);
+            nv = contrib_at(gv, grad_index(base, xi + c, yi + c), fc, fc, dx0, dy0, nv);
+            nv = contrib_at(gv, grad_index(base, xi + ec.a, yi + ec.b), ec.ox, ec.oy, dx0, dy0, nv);
         }
         acc[j] = fmaf(amp, nv * (1.0f / 47.0f), acc[j]);
     }
@@ -160,6 +150,13 @@ simplex2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) 
         const double xs_min = u0 + (u0 + (v0 + kTH * fr)) * kStretch;
         const double ys_min = v0 + ((u0 + kTW * fr) + v0) * kStretch;
         plan[threadIdx.x] = {floor(xs_min) - kTableMargin, floor(ys_min) - kTableMargin};
+    }
+    __shared__ ExtraCase ext[6];
+    if (threadIdx.x < 6) {
+        constexpr int ea[6] = {2, 0, 0, 1, -1, 1}, eb[6] = {0, 2, 0, -1, 1, 1};
+        const int i = threadIdx.x;
+        const float s = static_cast<float>(ea[i] + eb[i]) * static_cast<float>(kSquish);
+        ext[i] = {static_cast<float>(ea[i]) + s, static_cast<float>(eb[i]) + s, ea[i], eb[i]};
     }
     __shared__ float2 gv[8];  // (+-5, +-2) / (+-2, +-5): bit 0 swaps, bits 1 / 2 negate x / y
     if (threadIdx.x < 8) {
@@ -193,9 +190,9 @@ simplex2d_kernel(const __grid_constant__ FbmArgs args, float* __restrict__ out) 
         for (int o = 0; o < args.octaves; ++o) {
             const OctDev& od = args.oct[o];
             if (od.mode)
-                os_octave4<true>(acc, gv, od.ratio, od.amp, gtab + od.goff, od.ncx, plan[o].bx, plan[o].by, 0, gx, gy);
+                os_octave4<true>(acc, gv, ext, od.ratio, od.amp, gtab + od.goff, od.ncx, plan[o].bx, plan[o].by, 0, gx, gy);
             else
-                os_octave4<false>(acc, gv, od.ratio, od.amp, nullptr, 0, 0.0, 0.0, seed_key + od.oct_key, gx, gy);
+                os_octave4<false>(acc, gv, ext, od.ratio, od.amp, nullptr, 0, 0.0, 0.0, seed_key + od.oct_key, gx, gy);
         }
         const int64_t ly = ty0 + r0 + r - args.oy;
         if (ly >= 0 && ly < args.height) {
