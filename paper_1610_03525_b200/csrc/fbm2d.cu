@@ -625,6 +625,29 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             }
         }
     }
+    // Generic cells at the fixed in-cell positions of ppc 1 (x = y = 1/2) and
+    // ppc 2 (x, y in {1/4, 3/4}): the cell value is linear in its 12 corner
+    // values, so it is a fixed weighted sum — weights from the cell itself on
+    // one-hot corners (class 0: ppc 1; 1 + 2 iy + ix: ppc 2).
+    __shared__ float gwt[KIND == kGeneric ? 5 * 12 : 1];
+    if constexpr (KIND == kGeneric) {
+        if (tid < 5 * 12) {
+            const int cls = tid / 12, k = tid - cls * 12;
+            const float px = cls == 0 ? 0.5f : ((cls - 1) & 1) ? 0.75f : 0.25f;
+            const float py = cls == 0 ? 0.5f : ((cls - 1) & 2) ? 0.75f : 0.25f;
+            float k00[3], k10[3], k01[3], k11[3];  // the one-hot corner data (no local array)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                k00[c] = k == c ? 1.f : 0.f;
+                k10[c] = k == 3 + c ? 1.f : 0.f;
+                k01[c] = k == 6 + c ? 1.f : 0.f;
+                k11[c] = k == 9 + c ? 1.f : 0.f;
+            }
+            Cell<kGeneric> cw;
+            cw.make(k00, k10, k01, k11);
+            gwt[tid] = Cell<kGeneric>::eval(cw.row(py, 0.f), px, 0.f, 0.f);
+        }
+    }
     __syncthreads();
 
     // ---- evaluation of the thread's 4 x 8 pixels (no barriers) --------------
@@ -1240,6 +1263,92 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const TabSlot& tb = tabs[od.tslot];
             const float* g = grid + od.goff;
             const int pitch = od.pitch;
+            if constexpr (KIND == kGeneric) {
+                if (od.cls == kClsFast && (od.shift == 0 || od.shift == 1)) {
+                    // fixed positions: value = sum of the 12 corner values with the
+                    // class weights (gwt), no per-pixel cell set-up.  The thread's
+                    // corner rows are swept top to bottom (each corner value read
+                    // once per thread: 12 scattered loads per pixel were 4-way
+                    // bank-conflicted and saturated the shared-memory pipe).
+                    const int cx0 = tb.colI[c0];
+                    const int cy0 = __float_as_int(tb.rowF[r0].w);
+                    if (od.shift == 0) {
+                        float w[12];
+#pragma unroll
+                        for (int k = 0; k < 12; ++k) w[k] = gwt[k] * gscale;
+                        // corners (cx0 .. cx0 + 4) of a row, 3 channels
+                        auto load_row = [&](int cy, float (&v)[3][5]) {
+                            const int key = cy * pitch + cx0;
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                const float* q = g + c * kGridCap + key;
+                                const float4 t = *reinterpret_cast<const float4*>(q);  // cx0 % 4 == 0
+                                v[c][0] = t.x, v[c][1] = t.y, v[c][2] = t.z, v[c][3] = t.w;
+                                v[c][4] = q[4];
+                            }
+                        };
+                        float top[3][5], bot[3][5];
+                        load_row(cy0, top);
+#pragma unroll
+                        for (int r = 0; r < kRPT; ++r) {
+                            load_row(cy0 + r + 1, bot);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                float v = 0.f;
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                    v = fmaf(w[c], top[c][j], v);
+                                    v = fmaf(w[3 + c], top[c][j + 1], v);
+                                    v = fmaf(w[6 + c], bot[c][j], v);
+                                    v = fmaf(w[9 + c], bot[c][j + 1], v);
+                                }
+                                acc[r][j] += v;
+                            }
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                                for (int i = 0; i < 5; ++i) top[c][i] = bot[c][i];
+                        }
+                    } else {
+                        // ppc 2: corner columns cx0 .. cx0 + 2, cell rows of 2 pixel rows;
+                        // the pixel's class is its parity in the cell (even origins)
+                        auto load_row = [&](int cy, float (&v)[3][3]) {
+                            const int key = cy * pitch + cx0;
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                                for (int i = 0; i < 3; ++i) v[c][i] = gscale * g[c * kGridCap + key + i];
+                        };
+                        float top[3][3], bot[3][3];
+                        load_row(cy0, top);
+#pragma unroll
+                        for (int cr = 0; cr < kRPT / 2; ++cr) {
+                            load_row(cy0 + cr + 1, bot);
+#pragma unroll
+                            for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const float* w = gwt + 12 * (1 + 2 * rr + (j & 1));
+                                    const int cx = j >> 1;
+                                    float v = 0.f;
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c) {
+                                        v = fmaf(w[c], top[c][cx], v);
+                                        v = fmaf(w[3 + c], top[c][cx + 1], v);
+                                        v = fmaf(w[6 + c], bot[c][cx], v);
+                                        v = fmaf(w[9 + c], bot[c][cx + 1], v);
+                                    }
+                                    acc[2 * cr + rr][j] += v;
+                                }
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                                for (int i = 0; i < 3; ++i) top[c][i] = bot[c][i];
+                        }
+                    }
+                    continue;
+                }
+            }
             float x[4], sx[4], xs[4];
             int cxi[4];
 #pragma unroll
