@@ -503,6 +503,20 @@ def test_opensimplex_matches_restated_oracle(oracle, R, f0, octs, ratio):
     check_close(m.cpu().numpy(), oracle.generate(c, 0, 0, n), c, f"opensimplex R{R}")
 
 
+@pytest.mark.parametrize("R,f0,octs,pers,ox,oy,n", [
+    (512, 64, 5, 1.0, 0, 0, 256),          # persistence 1: fine octaves located per pixel (no stepping)
+    (256, 8, 8, 0.5, 0, 0, 256),           # fr up to 4: hashed octaves, stepped groups
+    (32768, 32, 16, 0.5, 31 * 1024, 30 * 1024, 200),  # far window (cell-aligned origin, the oracle's contract)
+    (4096, 8, 12, 0.5, 3584, 3584, 500),              # config 3's last tiles, partial pixel groups
+])
+def test_opensimplex_modes_and_far_windows(oracle, R, f0, octs, pers, ox, oy, n):
+    # fp32 lattice selection (region_case): near a region boundary the vertex that
+    # changes carries attn ~ 0, so the sum matches the fp64 oracle within tolerance
+    c = make_cfg(method=5, seed=31, resolution=R, base_frequency=f0, octaves=octs, persistence=pers)
+    m = gen(c, ox, oy, n)
+    check_close(m.cpu().numpy(), oracle.generate(c, ox, oy, n), c, f"opensimplex R{R} p{pers} @({ox},{oy})")
+
+
 def test_opensimplex_region_and_zero():
     c = make_cfg(method=5, seed=909, resolution=64, octaves=3)
     assert torch.equal(gen(c, 32, 32, 32), gen(c, 0, 0, 64)[32:, 32:])

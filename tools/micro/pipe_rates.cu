@@ -9,9 +9,10 @@ constexpr int kIters = 4096, kChains = 8;
 
 template <int OP>
 __global__ void rate(uint32_t* out, uint32_t seed) {
-    uint32_t a[kChains], b[kChains];
+    uint32_t a[kChains], b[kChains], ib[kChains];
+    const float2 m2 = make_float2(__uint_as_float(seed) * 0.5f, 0.999f), k2 = make_float2(1e-3f, __uint_as_float(seed));
 #pragma unroll
-    for (int c = 0; c < kChains; ++c) { a[c] = seed + threadIdx.x * 7 + c; b[c] = a[c] * 3u + 1u; }
+    for (int c = 0; c < kChains; ++c) { a[c] = seed + threadIdx.x * 7 + c; b[c] = a[c] * 3u + 1u; ib[c] = a[c]; }
     for (int i = 0; i < kIters; ++i) {
 #pragma unroll
         for (int c = 0; c < kChains; ++c) {
@@ -35,6 +36,28 @@ __global__ void rate(uint32_t* out, uint32_t seed) {
                 float f = __uint_as_float(a[c]), g = __uint_as_float(b[c]);
                 asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(f) : "f"(g));
                 a[c] = __float_as_uint(f);
+            } else if constexpr (OP == 7) {  // FFMA2 (fma.rn.f32x2): two fp32 FMAs per lane
+                float2 x = make_float2(__uint_as_float(a[c]), __uint_as_float(b[c]));
+                x = __ffma2_rn(x, m2, k2);
+                a[c] = __float_as_uint(x.x); b[c] = __float_as_uint(x.y);
+            } else if constexpr (OP == 8) {  // FFMA2 + IMAD interleaved (co-issue across pipes)
+                float2 x = make_float2(__uint_as_float(a[c]), __uint_as_float(b[c]));
+                x = __ffma2_rn(x, m2, k2);
+                a[c] = __float_as_uint(x.x); b[c] = __float_as_uint(x.y);
+                asm volatile("mad.lo.u32 %0, %0, 0x1A85EC53, %1;" : "+r"(ib[c]) : "r"(seed));
+            } else if constexpr (OP == 9) {  // FRND.F32.FLOOR
+                float f = __uint_as_float(a[c]);
+                asm volatile("cvt.rmi.f32.f32 %0, %0;" : "+f"(f));
+                a[c] = __float_as_uint(f) + 1u;
+            } else if constexpr (OP == 10) {  // FADD.RM (floor via 1.5 * 2^23)
+                float f = __uint_as_float(a[c]);
+                asm volatile("add.rm.f32 %0, %0, 0f4B400000;" : "+f"(f));
+                a[c] = __float_as_uint(f);
+            } else if constexpr (OP == 11) {  // FFMA + IMAD interleaved
+                float f = __uint_as_float(a[c]);
+                asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(f));
+                a[c] = __float_as_uint(f);
+                asm volatile("mad.lo.u32 %0, %0, 0x1A85EC53, %1;" : "+r"(b[c]) : "r"(a[c]));
             } else if constexpr (OP == 6) {  // mul.wide alone, both halves consumed
                 asm volatile("{.reg .b64 p; mul.wide.u32 p, %0, 0xED558CCD; mov.b64 {%0, %1}, p; xor.b32 %0, %0, %1;}"
                              : "+r"(a[c]), "=r"(b[c]));
@@ -43,7 +66,7 @@ __global__ void rate(uint32_t* out, uint32_t seed) {
     }
     uint32_t s = 0;
 #pragma unroll
-    for (int c = 0; c < kChains; ++c) s ^= a[c] ^ b[c];
+    for (int c = 0; c < kChains; ++c) s ^= a[c] ^ b[c] ^ ib[c];
     if (s == 0x12345678u) out[0] = s;
 }
 
@@ -81,5 +104,10 @@ int main() {
     run<4>("I2FP.F32.U32", 1);
     run<5>("FFMA 3-reg", 1);
     run<6>("IMAD.WIDE.U32 + LOP3", 2);
+    run<7>("FFMA2 (f32x2)", 1);
+    run<8>("FFMA2 + IMAD", 2);
+    run<9>("FRND.F32.FLOOR (+IADD)", 2);
+    run<10>("FADD.RM", 1);
+    run<11>("FFMA + IMAD", 2);
     return 0;
 }
