@@ -1203,17 +1203,33 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             }
             // row terms: the column-independent one to the row accumulator,
             // the rest 3 FFMA per pixel (Perlin {x, sx, xs}, generic Horner in x)
+            // column pairs (0, 1), (2, 3) in packed fp32x2 (FFMA2: one issue slot
+            // per pair, each lane rounded as fmaf — bit-identical)
+            const float2 x2[2] = {make_float2(x[0], x[1]), make_float2(x[2], x[3])};
+            const float2 sx2[2] = {make_float2(sx[0], sx[1]), make_float2(sx[2], sx[3])};
+            const float2 xs2[2] = {make_float2(xs[0], xs[1]), make_float2(xs[2], xs[3])};
             auto accum = [&](int r, const typename Cell<KIND>::Row& row) {
                 if constexpr (KIND == kPerlin) {
                     racc[r] += row.a0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        acc[r][j] = fmaf(xs[j], row.a3, fmaf(sx[j], row.a2, fmaf(x[j], row.a1, acc[r][j])));
+                    for (int p = 0; p < 2; ++p) {
+                        float2 a = make_float2(acc[r][2 * p], acc[r][2 * p + 1]);
+                        a = __ffma2_rn(x2[p], make_float2(row.a1, row.a1), a);
+                        a = __ffma2_rn(sx2[p], make_float2(row.a2, row.a2), a);
+                        a = __ffma2_rn(xs2[p], make_float2(row.a3, row.a3), a);
+                        acc[r][2 * p] = a.x;
+                        acc[r][2 * p + 1] = a.y;
+                    }
                 } else if constexpr (KIND == kGeneric) {
                     racc[r] += row.r0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        acc[r][j] = fmaf(fmaf(fmaf(row.r3, x[j], row.r2), x[j], row.r1), x[j], acc[r][j]);
+                    for (int p = 0; p < 2; ++p) {
+                        float2 t = __ffma2_rn(make_float2(row.r3, row.r3), x2[p], make_float2(row.r2, row.r2));
+                        t = __ffma2_rn(t, x2[p], make_float2(row.r1, row.r1));
+                        const float2 a = __ffma2_rn(t, x2[p], make_float2(acc[r][2 * p], acc[r][2 * p + 1]));
+                        acc[r][2 * p] = a.x;
+                        acc[r][2 * p + 1] = a.y;
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) acc[r][j] += Cell<KIND>::eval(row, x[j], sx[j], xs[j]);
@@ -1292,17 +1308,35 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
 #pragma unroll
                         for (int r = 0; r < kRPT; ++r) {
                             load_row(cy0 + r + 1, bot);
+                            // v_j = A_j + B_(j+1): A_i = sum_c w_c top_c[i] + w_(6+c) bot_c[i] (corner
+                            // column i as a cell's left corners), B_i the same with w_(3+c), w_(9+c)
+                            // (as its right corners); column pairs (0, 1), (2, 3) in FFMA2
+                            float2 A[2], B[2];
+                            float B4 = 0.f;
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                float v = 0.f;
+                            for (int p = 0; p < 2; ++p) {
+                                A[p] = B[p] = make_float2(0.f, 0.f);
 #pragma unroll
                                 for (int c = 0; c < 3; ++c) {
-                                    v = fmaf(w[c], top[c][j], v);
-                                    v = fmaf(w[3 + c], top[c][j + 1], v);
-                                    v = fmaf(w[6 + c], bot[c][j], v);
-                                    v = fmaf(w[9 + c], bot[c][j + 1], v);
+                                    const float2 tp = make_float2(top[c][2 * p], top[c][2 * p + 1]);
+                                    const float2 bp = make_float2(bot[c][2 * p], bot[c][2 * p + 1]);
+                                    A[p] = __ffma2_rn(make_float2(w[c], w[c]), tp, A[p]);
+                                    A[p] = __ffma2_rn(make_float2(w[6 + c], w[6 + c]), bp, A[p]);
+                                    B[p] = __ffma2_rn(make_float2(w[3 + c], w[3 + c]), tp, B[p]);
+                                    B[p] = __ffma2_rn(make_float2(w[9 + c], w[9 + c]), bp, B[p]);
                                 }
-                                acc[r][j] += v;
+                            }
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                B4 = fmaf(w[3 + c], top[c][4], B4);
+                                B4 = fmaf(w[9 + c], bot[c][4], B4);
+                            }
+                            const float Bn[4] = {B[0].y, B[1].x, B[1].y, B4};
+#pragma unroll
+                            for (int p = 0; p < 2; ++p) {
+                                const float2 a = __fadd2_rn(make_float2(acc[r][2 * p], acc[r][2 * p + 1]), A[p]);
+                                acc[r][2 * p] = a.x + Bn[2 * p];
+                                acc[r][2 * p + 1] = a.y + Bn[2 * p + 1];
                             }
 #pragma unroll
                             for (int c = 0; c < 3; ++c)

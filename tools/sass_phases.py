@@ -41,6 +41,7 @@ iE, iS = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All
 data = [r for r in rows[2:] if len(r) > iE and r[iE].isdigit()]
 base = int(data[0][0], 16)
 byop, byline, st = collections.Counter(), collections.Counter(), collections.Counter()
+fpline = collections.Counter()  # FFMA / FADD / FMUL per line (candidates for fp32x2 packing)
 tot = 0
 for r in data:
     n, s = int(r[iE]), int(r[iS] or 0)
@@ -50,6 +51,8 @@ for r in data:
     byop[op] += n
     byline[loc] += n
     st[loc] += s
+    if op in ("FFMA", "FADD", "FMUL"):
+        fpline[loc] += n
     tot += n
 print("executed warp instructions:", tot)
 print(" ".join(f"{k}:{v / tot * 100:.1f}%" for k, v in byop.most_common(14)))
@@ -59,6 +62,14 @@ for loc, v in byline.most_common(nlines):
     f, ln = loc
     s = text.get(f, [""] * (ln + 1))[ln - 1].strip()[:88] if f else "?"
     print(f"{v:9d} {v / tot * 100:5.1f}% st{st[loc]:5d} {str(f)[:6]}:{ln:4d} {s}")
+
+if "--fp" in sys.argv:
+    fpt = sum(fpline.values())
+    print(f"scalar fp32 (FFMA/FADD/FMUL): {fpt} = {fpt / tot * 100:.1f}%")
+    for loc, v in fpline.most_common(nlines):
+        f, ln = loc
+        s = text.get(f, [""] * (ln + 1))[ln - 1].strip()[:88] if f else "?"
+        print(f"{v:9d} {v / tot * 100:5.1f}% {str(f)[:6]}:{ln:4d} {s}")
 
 # --- optional: sum by kernel phase, delimited by marker comments in fbm2d.cu
 if "--phases" in sys.argv:
