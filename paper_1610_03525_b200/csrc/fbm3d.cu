@@ -73,6 +73,40 @@ __device__ __forceinline__ uint64_t pack3(uint64_t base, int64_t ix, int64_t iy,
 
 __device__ __forceinline__ float lerp(float a, float b, float s) { return fmaf(s, b - a, a); }
 
+// Column pairs (0, 1), (2, 3) of a row accumulated in packed fp32x2 (FFMA2 /
+// FADD2: one issue slot per pair, each lane rounded as the scalar op).
+#ifndef TG_F32X2_3D
+#define TG_F32X2_3D 1
+#endif
+__device__ __forceinline__ void fma4(float (&a)[4], const float (&x)[4], float y) {
+#if TG_F32X2_3D
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const float2 r = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), make_float2(y, y),
+                                    make_float2(a[2 * p], a[2 * p + 1]));
+        a[2 * p] = r.x;
+        a[2 * p + 1] = r.y;
+    }
+#else
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] = fmaf(x[j], y, a[j]);
+#endif
+}
+__device__ __forceinline__ void fma4s(float (&a)[4], float x, const float (&y)[4]) {
+#if TG_F32X2_3D
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const float2 r = __ffma2_rn(make_float2(x, x), make_float2(y[2 * p], y[2 * p + 1]),
+                                    make_float2(a[2 * p], a[2 * p + 1]));
+        a[2 * p] = r.x;
+        a[2 * p + 1] = r.y;
+    }
+#else
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] = fmaf(x, y[j], a[j]);
+#endif
+}
+
 // One plan entry per octave is computed by the host (capi.cu plan3):
 // mode in OctDev.mode, grid shape ncx, ncy, pad(=ncz), pitch (x stride), goff.
 enum Mode3 : int32_t { kM3Sub = 0, kM3P1 = 1, kM3Blk = 2, kM3Gen = 3, kM3Direct = 4 };
@@ -268,11 +302,9 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                 }
                 float h[8];
                 map_heightN<8>(p, h);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    acc[z][j] = fmaf(amp, h[j], acc[z][j]);
-                    acc[z + 1][j] = fmaf(amp, h[4 + j], acc[z + 1][j]);
-                }
+                const float h0[4] = {h[0], h[1], h[2], h[3]}, h1[4] = {h[4], h[5], h[6], h[7]};
+                fma4s(acc[z], amp, h0);
+                fma4s(acc[z + 1], amp, h1);
                 if (z + 2 < kTZ) K = add64(p[4], kz);
             }
             continue;
@@ -299,11 +331,16 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
             for (int z = 0; z < kTZ; ++z) {
                 float Fb[4];
                 face(z + 1, Fb);
+                float Fs[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    acc[z][j] = fmaf(q, Fa[j] + Fb[j], acc[z][j]);
-                    Fa[j] = Fb[j];
+                for (int p = 0; p < 2; ++p) {
+                    const float2 t = __fadd2_rn(make_float2(Fa[2 * p], Fa[2 * p + 1]), make_float2(Fb[2 * p], Fb[2 * p + 1]));
+                    Fs[2 * p] = t.x;
+                    Fs[2 * p + 1] = t.y;
                 }
+                fma4s(acc[z], q, Fs);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) Fa[j] = Fb[j];
             }
             continue;
         }
@@ -360,8 +397,7 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                         const float sz = szv[z];
                         const float b0 = lerp(e0, e1, sz), d = lerp(e2, e3, sz) - b0;
                         racc[z] += b0;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) acc[z][j] = fmaf(sx[j], d, acc[z][j]);
+                        fma4(acc[z], sx, d);
                     }
                 }
             } else {
@@ -384,10 +420,24 @@ fbm3d_kernel(const __grid_constant__ Fbm3Args a, float* __restrict__ out) {
                         const float b0 = lerp(e[0][0], e[0][1], sz);
                         const float b1 = lerp(e[1][0], e[1][1], sz);
                         const float b2 = lerp(e[2][0], e[2][1], sz);
+#if TG_F32X2_3D
+                        // columns (0, 1) lerp b0 -> b1, (2, 3) b1 -> b2 (x = 1/4, 3/4)
+                        const float2 sxp = make_float2(sx[0], sx[1]);
+                        const float d01 = b1 - b0, d12 = b2 - b1;
+                        const float2 l0 = __ffma2_rn(sxp, make_float2(d01, d01), make_float2(b0, b0));
+                        const float2 l1 = __ffma2_rn(sxp, make_float2(d12, d12), make_float2(b1, b1));
+                        const float2 s0 = __fadd2_rn(make_float2(acc[z][0], acc[z][1]), l0);
+                        const float2 s1 = __fadd2_rn(make_float2(acc[z][2], acc[z][3]), l1);
+                        acc[z][0] = s0.x;
+                        acc[z][1] = s0.y;
+                        acc[z][2] = s1.x;
+                        acc[z][3] = s1.y;
+#else
                         acc[z][0] += lerp(b0, b1, sx[0]);
                         acc[z][1] += lerp(b0, b1, sx[1]);
                         acc[z][2] += lerp(b1, b2, sx[2]);
                         acc[z][3] += lerp(b1, b2, sx[3]);
+#endif
                     }
                 }
             }

@@ -17,7 +17,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, sym = sys.argv[1], sys.argv[2]
 nlines = int(sys.argv[sys.argv.index("--lines") + 1]) if "--lines" in sys.argv else 30
-src_file = os.path.join(ROOT, "paper_1610_03525_b200", "csrc", "fbm2d.cu")
+src_name = sys.argv[sys.argv.index("--src") + 1] if "--src" in sys.argv else "fbm2d.cu"
+src_file = os.path.join(ROOT, "paper_1610_03525_b200", "csrc", src_name)
 subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                 "--expt-relaxed-constexpr", "-cubin", "-o", "/tmp/_k.cubin", src_file], check=True)
 sass = subprocess.run(["nvdisasm", "-gi", "/tmp/_k.cubin"], capture_output=True, text=True).stdout.split("\n")
@@ -57,7 +58,7 @@ for r in data:
 print("executed warp instructions:", tot)
 print(" ".join(f"{k}:{v / tot * 100:.1f}%" for k, v in byop.most_common(14)))
 text = {f: open(os.path.join(ROOT, "paper_1610_03525_b200", "csrc", f)).read().split("\n")
-        for f in ("fbm2d.cu", "lattice.cuh")}
+        for f in (src_name, "lattice.cuh")}
 for loc, v in byline.most_common(nlines):
     f, ln = loc
     s = text.get(f, [""] * (ln + 1))[ln - 1].strip()[:88] if f else "?"
