@@ -31,6 +31,25 @@
 #include <type_traits>
 
 #include "devattr.h"
+
+// FFMA2 / FADD2 column pairs (bit-identical per lane) in the lattice-point,
+// ppc-2 and ppc-1 zero-gradient octaves (config 2: 51.2 -> 50.2 us); the
+// pixel formation of the separated form too would exceed 64 registers.
+#ifndef TG_F2_SUB
+#define TG_F2_SUB 1
+#endif
+#ifndef TG_F2_PPC2
+#define TG_F2_PPC2 1
+#endif
+#ifndef TG_F2_PPC1
+#define TG_F2_PPC1 1
+#endif
+#ifndef TG_F2_BLK
+#define TG_F2_BLK 1
+#endif
+#ifndef TG_F2_FORM
+#define TG_F2_FORM 0
+#endif
 #include "fbm_params.h"
 #include "lattice.cuh"
 
@@ -270,6 +289,51 @@ struct Ppc4S {
     static constexpr float D(int i) { return static_cast<float>(Sd(i) - (2.0 * i + 1.0) / 8.0); }
 };
 
+// acc[j] += m * h[j] for the four columns, as two FFMA2 (column pairs;
+// each lane rounds exactly as fmaf(m, h[j], acc[j])).
+__device__ __forceinline__ void fma_pairs(float (&acc)[4], const float* h, float m) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const float2 a = __ffma2_rn(make_float2(h[2 * p], h[2 * p + 1]), make_float2(m, m),
+                                    make_float2(acc[2 * p], acc[2 * p + 1]));
+        acc[2 * p] = a.x;
+        acc[2 * p + 1] = a.y;
+    }
+}
+
+// Separated-form terms of one block octave (zg paper, ppc >= 8) in FFMA2
+// pairs, each lane rounded as the scalar form:
+//   C0[j] = fmaf(D[j], ay0, fmaf(S[j], dx, C0[j])), C1[j] = fmaf(D[j], ad, C1[j]),
+//   R0[r] = fmaf(Sy[r], k0, R0[r]),                 R1[r] = fmaf(Sy[r], ad, R1[r]).
+template <class SyLoad>
+__device__ __forceinline__ void sep_terms(float (&C0)[4], float (&C1)[4], float (&R0)[kRPT], float (&R1)[kRPT],
+                                          float4 sx, float4 dd, float dx, float ay0, float ad, float k0,
+                                          SyLoad sy_load) {
+    const float2 S2[2] = {make_float2(sx.x, sx.y), make_float2(sx.z, sx.w)};
+    const float2 D2[2] = {make_float2(dd.x, dd.y), make_float2(dd.z, dd.w)};
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        float2 c0 = __ffma2_rn(S2[p], make_float2(dx, dx), make_float2(C0[2 * p], C0[2 * p + 1]));
+        c0 = __ffma2_rn(D2[p], make_float2(ay0, ay0), c0);
+        const float2 c1 = __ffma2_rn(D2[p], make_float2(ad, ad), make_float2(C1[2 * p], C1[2 * p + 1]));
+        C0[2 * p] = c0.x, C0[2 * p + 1] = c0.y;
+        C1[2 * p] = c1.x, C1[2 * p + 1] = c1.y;
+    }
+#pragma unroll
+    for (int r4 = 0; r4 < kRPT; r4 += 4) {
+        const float4 sy = sy_load(r4);
+        const float2 Y2[2] = {make_float2(sy.x, sy.y), make_float2(sy.z, sy.w)};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int r = r4 + 2 * p;
+            const float2 a = __ffma2_rn(Y2[p], make_float2(k0, k0), make_float2(R0[r], R0[r + 1]));
+            const float2 b = __ffma2_rn(Y2[p], make_float2(ad, ad), make_float2(R1[r], R1[r + 1]));
+            R0[r] = a.x, R0[r + 1] = a.y;
+            R1[r] = b.x, R1[r + 1] = b.y;
+        }
+    }
+}
+
 // q*((h00 + h10) + (h01 + h11)) over a 4 x 8 pixel block whose corners are
 // rows r = 0..8 of a 5-wide corner strip: x = y = 0.5 makes every zero-
 // gradient kernel (S3 or S5, paper or separable) the mean of its 4 corners
@@ -284,10 +348,21 @@ __device__ __forceinline__ void ppc1_block(float (&acc)[kRPT][4], float q, Fetch
         fetch(r + 1, h);
         const float ns[4] = {h[0] + h[1], h[1] + h[2], h[2] + h[3], h[3] + h[4]};
 #pragma unroll
+#if TG_F2_PPC1
+        for (int p = 0; p < 2; ++p) {  // column pairs in FADD2 / FFMA2 (each lane as before)
+            const float2 s = __fadd2_rn(make_float2(hs[2 * p], hs[2 * p + 1]), make_float2(ns[2 * p], ns[2 * p + 1]));
+            const float2 a = __ffma2_rn(make_float2(q, q), s, make_float2(acc[r][2 * p], acc[r][2 * p + 1]));
+            acc[r][2 * p] = a.x;
+            acc[r][2 * p + 1] = a.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hs[j] = ns[j];
+#else
         for (int j = 0; j < 4; ++j) {
             acc[r][j] = fmaf(q, hs[j] + ns[j], acc[r][j]);
             hs[j] = ns[j];
         }
+#endif
     }
 }
 
@@ -794,6 +869,11 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const float sxa[4] = {sx.x, sx.y, sx.z, sx.w}, dda[4] = {dd.x, dd.y, dd.z, dd.w};
             const float ay0 = a * y0, ad = a * inv, k0 = fmaf(a, x0, dy);
             hsum += h00;
+#if TG_F2_BLK
+            sep_terms(C0, C1, R0, R1, sx, dd, dx, ay0, ad, k0, [&](int r4) {
+                return __ldg(reinterpret_cast<const float4*>(lutS + PPC + my + r4));
+            });
+#else
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 C0[j] = fmaf(dda[j], ay0, fmaf(sxa[j], dx, C0[j]));
@@ -809,6 +889,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                     R1[r4 + i] = fmaf(sya[i], ad, R1[r4 + i]);
                 }
             }
+#endif
         };
         blk_slot(std::integral_constant<int, 4>{});
         blk_slot(std::integral_constant<int, 3>{});
@@ -829,6 +910,11 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             const float sxa[4] = {sx.x, sx.y, sx.z, sx.w}, dda[4] = {dd.x, dd.y, dd.z, dd.w};
             const float ay0 = a * y0, ad = a * inv, k0 = fmaf(a, x0, dy);
             hsum += h00;
+#if TG_F2_BLK
+            sep_terms(C0, C1, R0, R1, sx, dd, dx, ay0, ad, k0, [&](int r4) {
+                return __ldg(reinterpret_cast<const float4*>(lutS + od.ppc + my + r4));
+            });
+#else
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 C0[j] = fmaf(dda[j], ay0, fmaf(sxa[j], dx, C0[j]));
@@ -844,6 +930,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                     R1[r4 + i] = fmaf(sya[i], ad, R1[r4 + i]);
                 }
             }
+#endif
         }
         // ppc == 4 in the same separated form.  The thread's 4 columns are one
         // cell (x = 1/8 + c/4); rows 0-3 lie in cell row A, rows 4-7 in B
@@ -924,6 +1011,24 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
             CB[j] = CA[j] + D0[j];
             C1B[j] = C1[j] + D1[j];
         }
+#if TG_F2_FORM
+#pragma unroll
+        for (int r = 0; r < kRPT; ++r) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {  // column pairs (2p, 2p + 1) in FADD2 / FFMA2
+                const float* cc = r >= 4 ? CB : CA;
+                const float* c1 = r >= 4 ? C1B : C1;
+                float2 v = __fadd2_rn(make_float2(cc[2 * p], cc[2 * p + 1]), make_float2(R0[r], R0[r]));
+                if (r) v = __ffma2_rn(make_float2(static_cast<float>(r), static_cast<float>(r)),
+                                      make_float2(c1[2 * p], c1[2 * p + 1]), v);
+                // column 0 adds 0 * R1 (= v up to the sign of a zero)
+                v = __ffma2_rn(make_float2(static_cast<float>(2 * p), static_cast<float>(2 * p + 1)),
+                               make_float2(R1[r], R1[r]), v);
+                acc[r][2 * p] = v.x;
+                acc[r][2 * p + 1] = v.y;
+            }
+        }
+#else
 #pragma unroll
         for (int r = 0; r < kRPT; ++r) {
 #pragma unroll
@@ -934,6 +1039,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 acc[r][j] = v;
             }
         }
+#endif
     } else {
         const float init = KIND == kGeneric ? hsum : 0.f;  // zg separable folds hsum later
 #pragma unroll
@@ -1021,6 +1127,22 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
 #pragma unroll
                 for (int u = 0; u < 3; ++u) b[u] = gn[u];
 #pragma unroll
+#if TG_F2_PPC2
+                for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        // pixel pair (2 cc, 2 cc + 1) = cell positions ix = 0, 1:
+                        // per-lane weights, shared corner (FFMA2, each lane as fmaf)
+                        using W = Ppc2W<KIND, ORDER>;
+                        float2 a = make_float2(acc[2 * k + iy][2 * cc], acc[2 * k + iy][2 * cc + 1]);
+                        a = __ffma2_rn(make_float2(W::w(0, iy, 3), W::w(1, iy, 3)), make_float2(b[cc + 1], b[cc + 1]), a);
+                        a = __ffma2_rn(make_float2(W::w(0, iy, 2), W::w(1, iy, 2)), make_float2(b[cc], b[cc]), a);
+                        a = __ffma2_rn(make_float2(W::w(0, iy, 1), W::w(1, iy, 1)), make_float2(t[cc + 1], t[cc + 1]), a);
+                        a = __ffma2_rn(make_float2(W::w(0, iy, 0), W::w(1, iy, 0)), make_float2(t[cc], t[cc]), a);
+                        acc[2 * k + iy][2 * cc] = a.x;
+                        acc[2 * k + iy][2 * cc + 1] = a.y;
+                    }
+#else
                 for (int iy = 0; iy < 2; ++iy)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
@@ -1031,6 +1153,7 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                         a = fmaf(Ppc2W<KIND, ORDER>::w(ix, iy, 1), t[cc + 1], a);
                         a = fmaf(Ppc2W<KIND, ORDER>::w(ix, iy, 0), t[cc], a);
                     }
+#endif
 #pragma unroll
                 for (int u = 0; u < 3; ++u) t[u] = b[u];
             }
@@ -1168,9 +1291,13 @@ fbm2d_kernel(const __grid_constant__ FbmArgs args, const __grid_constant__ CUten
                 float h[4 * TG_SUB_ROWS];
                 map_heightN<4 * TG_SUB_ROWS>(p, h);
 #pragma unroll
+#if TG_F2_SUB
+                for (int i = 0; i < TG_SUB_ROWS; ++i) fma_pairs(acc[r + i], h + 4 * i, amp);
+#else
                 for (int i = 0; i < TG_SUB_ROWS; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) acc[r + i][j] = fmaf(amp, h[4 * i + j], acc[r + i][j]);
+#endif
                 if (r + TG_SUB_ROWS < kRPT) K = add64(p[4 * (TG_SUB_ROWS - 1)], ky);
             }
 #endif
