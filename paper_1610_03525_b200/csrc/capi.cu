@@ -16,6 +16,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -753,11 +754,6 @@ double env_double(const char* name, double dflt) {
 
 }  // namespace
 
-// Host widening cost (ns per element, running average over calls) and the
-// PCIe time of one fp32 element at ~52 GB/s (D2H on the B200 host).
-static std::atomic<double> g_widen_ns_per_elem{0.0};
-constexpr double kPcieNsPerF32 = 4.0 / 52.0;
-
 static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64_t extent,
                          void* host_out, uint64_t n_out, bool f64) {
     if (int st = validate_cfg(cfg)) return st;
@@ -786,18 +782,12 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     // 1.5-1.6 ms vs 2.45 ms device-widened), all-device otherwise.  Pageable
     // destinations always take the host route (a pageable DMA is
     // driver-staged anyway).
-    // Adaptive split for pinned f64 destinations: with P = PCIe time of an
-    // fp32 band and H = host widening time of a band (running average over
-    // calls), host-widening a fraction f of the bands costs
-    // max((2 - f) P, f H) per band, minimal at f = 2P / (P + H): all-host
-    // while the host keeps up (H <= P), shifting bands to device widening
-    // when the host's memory bandwidth is contended (measured bimodal on the
-    // shared B200 host: 1.38 vs 2.1-2.3 ms all-host at config 2).
-    double frac_dflt = 0.0;
-    if (tg::host::threads() >= 4) {
-        const double h = g_widen_ns_per_elem.load(std::memory_order_relaxed);
-        frac_dflt = h > 0.0 ? std::min(1.0, 2.0 * kPcieNsPerF32 / (kPcieNsPerF32 + h)) : 1.0;
-    }
+    // Mixing the two routes per band (host-widening a fraction 2P / (P + H)
+    // of the bands, P / H the PCIe / host time of a band) measured no better
+    // than all-host even when the host was the slower side (B200 host,
+    // 1.98 ms all-host vs 2.06-2.28 ms at fractions 0.875-0.5): the f64 DMA
+    // slows the host workers as much as it relieves them.
+    const double frac_dflt = tg::host::threads() >= 4 ? 1.0 : 0.0;
     double frac = f64 ? (pinned ? env_double("TG_HOST_WIDEN_FRAC", frac_dflt) : 1.0) : 1.0;
     frac = std::min(1.0, std::max(0.0, frac));
     auto host_widened = [&](int64_t i) {
@@ -808,8 +798,15 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     if (!s) return fail(TG_EDEVICE, "generate: staging allocation failed");
 
     int rc = TG_OK;
+    constexpr int ns = kSlots;  // a ring as deep as the map (DMA never throttled) measured the same
+    const bool dbg = env_flag("TG_HOST_DEBUG", false);
+    // workers poll between bands for the length of this call (direct fp32
+    // DMA into a pinned destination has no host work)
+    std::unique_ptr<tg::host::Burst> burst;
+    if (!direct32 && env_flag("TG_HOST_SPIN", true)) burst.reset(new tg::host::Burst);
     auto drain = [&](int64_t j) {
-        const int slot = static_cast<int>(j % kSlots);
+        const int slot = static_cast<int>(j % ns);
+        const auto tw0 = std::chrono::steady_clock::now();
         if (cudaError_t e = cudaEventSynchronize(s->ev[slot])) {
             if (rc == TG_OK) rc = cuda_fail(e, "generate_host");
             return;
@@ -821,12 +818,10 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
         if (f64) {
             const auto t0 = std::chrono::steady_clock::now();
             tg::host::widen(s->pin[slot], static_cast<double*>(host_out) + off, n, nt);
-            const double ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
-            if (n >= (size_t(1) << 18)) {  // running average of the host widening cost
-                const double prev = g_widen_ns_per_elem.load(std::memory_order_relaxed);
-                const double cur = ns / static_cast<double>(n);
-                g_widen_ns_per_elem.store(prev > 0.0 ? 0.75 * prev + 0.25 * cur : cur, std::memory_order_relaxed);
-            }
+            if (dbg)  // TG_HOST_DEBUG=1: per band, the wait for its copy and the widening time
+                std::fprintf(stderr, "band %lld wait %.1f us widen %.1f us\n", static_cast<long long>(j),
+                             std::chrono::duration<double, std::micro>(t0 - tw0).count(),
+                             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
         }
         else tg::host::copy(s->pin[slot], static_cast<float*>(host_out) + off, n, nt);
     };
@@ -834,7 +829,7 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     int64_t issued = 0;
     for (int64_t i = 0; i < nb && rc == TG_OK; ++i) {
         const int64_t y0 = i * band, h = std::min<int64_t>(band, extent - y0);
-        const int b = static_cast<int>(i & 1), slot = static_cast<int>(i % kSlots);
+        const int b = static_cast<int>(i & 1), slot = static_cast<int>(i % ns);
         if (build_args(cfg, ox, oy + y0, extent, h, extent, &a) != TG_OK) {
             rc = TG_EDEVICE;
             break;
@@ -859,9 +854,9 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
             break;
         }
         issued = i + 1;
-        if (i >= kSlots - 1) drain(i - (kSlots - 1));
+        if (i >= ns - 1) drain(i - (ns - 1));
     }
-    for (int64_t j = std::max<int64_t>(0, issued - (kSlots - 1)); j < issued; ++j) drain(j);
+    for (int64_t j = std::max<int64_t>(0, issued - (ns - 1)); j < issued; ++j) drain(j);
     for (auto st : s->st) {
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess && rc == TG_OK) rc = cuda_fail(e, "generate_host sync");

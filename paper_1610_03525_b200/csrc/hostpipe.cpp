@@ -32,6 +32,19 @@ class Pool {
     }
     int size() const { return n_; }
 
+    // Between begin_burst() and end_burst() idle workers poll for the next
+    // job instead of sleeping on the condition variable: a futex wake of an
+    // idle (halted) virtual CPU costs 50-130 us on the B200 host, once per
+    // band and worker, which doubled the widening time of an 8 MiB band.
+    void begin_burst() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            hot_.fetch_add(1, std::memory_order_release);
+        }
+        cv_.notify_all();
+    }
+    void end_burst() { hot_.fetch_sub(1, std::memory_order_release); }
+
     void run(int n, const std::function<void(int)>& f) {
         std::lock_guard<std::mutex> submit(submit_);
         if (n_ <= 1 || n <= 1) {
@@ -44,10 +57,15 @@ class Pool {
         {
             std::lock_guard<std::mutex> lk(m_);
             job_ = job;
-            ++gen_;
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
         work(*job);
+        if (hot_.load(std::memory_order_acquire) > 0) {
+            // the stragglers are mid-piece: poll, they finish within microseconds
+            for (int spins = 0; job->done.load(std::memory_order_acquire) != n && spins < (1 << 22); ++spins)
+                _mm_pause();
+        }
         std::unique_lock<std::mutex> lk(m_);
         done_cv_.wait(lk, [&] { return job->done.load() == n; });
         job_.reset();
@@ -76,11 +94,19 @@ class Pool {
     void loop() {
         uint64_t seen = 0;
         for (;;) {
+            // next job: poll while a burst is open, sleep otherwise
+            while (gen_.load(std::memory_order_acquire) == seen) {
+                if (hot_.load(std::memory_order_acquire) > 0) {
+                    _mm_pause();
+                    continue;
+                }
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_.load() != seen || hot_.load() > 0; });
+            }
             std::shared_ptr<Job> j;
             {
-                std::unique_lock<std::mutex> lk(m_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
+                std::lock_guard<std::mutex> lk(m_);
+                seen = gen_.load();
                 j = job_;
             }
             if (j) work(*j);
@@ -91,22 +117,23 @@ class Pool {
     std::mutex submit_, m_;
     std::condition_variable cv_, done_cv_;
     std::shared_ptr<Job> job_;
-    uint64_t gen_ = 0;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> hot_{0};
 };
 
 Pool& pool() {
     static Pool* p = [] {
-        // Streaming widen/copy is host-memory-bound: on the B200 host (16
-        // hardware threads) 5-6 workers run fastest (f64 drop-in 1.5-1.6 ms),
-        // 8 already slower (2.0-2.4 ms) and 12 collapse (7-10 ms) as they
-        // contend with the CUDA driver and the caller for the same cores
-        // (tools/time_e2e.py).  Default: half the hardware threads minus two,
-        // shared among the ranks of this node (LOCAL_WORLD_SIZE, set by
-        // torchrun), at most 6.
+        // Streaming widen/copy: workers are bound by the latency of reading
+        // the freshly DMA-written bands, so more of them help up to about
+        // half the hardware threads (B200 host, 16 threads, config 2 f64
+        // drop-in with DMA in flight: 4 workers 2.86 ms, 6: 2.29-2.69, 8:
+        // 2.07-2.53, 10: 1.93-2.37; the rest stay free for the CUDA driver
+        // and the caller).  Shared among the ranks of this node
+        // (LOCAL_WORLD_SIZE, set by torchrun), at most 8.
         int n = static_cast<int>(std::thread::hardware_concurrency());
         int ranks = 1;
         if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, std::atoi(e));
-        n = std::min(std::max((n / 2 - 2) / ranks, 1), 6);
+        n = std::min(std::max((n / 2) / ranks, 1), 8);
         if (const char* e = std::getenv("TG_HOST_THREADS")) n = std::max(1, std::atoi(e));
         return new Pool(n);
     }();
@@ -119,7 +146,14 @@ Pool& pool() {
 __attribute__((target("avx512f"))) void widen_avx512(const float* s, double* d, size_t n) {
     size_t i = 0;
     for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 63); ++i) d[i] = s[i];
+    // The source is a band the copy engine has just written: its lines come
+    // from memory (or the IO agent's cache) at a latency the hardware
+    // streamer, restarting at every 4 KiB page, does not cover while DMA is
+    // still running; an L2 prefetch 16 KiB ahead does (B200 host, config 2,
+    // 6 workers: 2.2 -> 2.0 ms; 10 workers 1.93 -> 1.80 ms).
+    static const int pf = [] { const char* e = std::getenv("TG_HOST_PREFETCH"); return e ? std::atoi(e) : 16384; }();
     for (; i + 16 <= n; i += 16) {
+        if (pf) _mm_prefetch(reinterpret_cast<const char*>(s + i) + pf, _MM_HINT_T1);
         const __m512 a = _mm512_loadu_ps(s + i);
         _mm512_stream_pd(d + i, _mm512_cvtps_pd(_mm512_castps512_ps256(a)));
         _mm512_stream_pd(d + i + 8, _mm512_cvtps_pd(_mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castps_pd(a), 1))));
@@ -168,12 +202,19 @@ void copy_serial(const float* s, float* d, size_t n, bool stream) {
     std::memcpy(d, s, n * sizeof(float));
 }
 
+#ifndef TG_HOST_PIECES
+#define TG_HOST_PIECES 4
+#endif
+constexpr size_t kPiecesPerWorker = TG_HOST_PIECES;
+
 template <class F>
 void split(size_t n, F&& f) {
     const int t = pool().size();
     // >= 64 KiB of input per piece, pieces on 64-element boundaries
     const size_t min_piece = 16384;
-    int pieces = static_cast<int>(std::min<size_t>(static_cast<size_t>(t), (n + min_piece - 1) / min_piece));
+    // a few pieces per worker (dynamic hand-out): a worker that starts late
+    // or shares its core does not hold the whole band back
+    int pieces = static_cast<int>(std::min<size_t>(static_cast<size_t>(t) * kPiecesPerWorker, (n + min_piece - 1) / min_piece));
     pieces = std::max(pieces, 1);
     size_t per = (n + pieces - 1) / pieces;
     per = (per + 63) / 64 * 64;
@@ -187,6 +228,9 @@ void split(size_t n, F&& f) {
 }  // namespace
 
 int threads() { return pool().size(); }
+
+Burst::Burst() { pool().begin_burst(); }
+Burst::~Burst() { pool().end_burst(); }
 
 void parallel_for(int n, const std::function<void(int)>& f) { pool().run(n, f); }
 

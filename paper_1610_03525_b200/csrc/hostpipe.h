@@ -17,6 +17,16 @@ int threads();
 // all are done.  Calls from different threads are serialised.
 void parallel_for(int n, const std::function<void(int)>& f);
 
+// While a Burst is alive the pool's idle workers poll for the next job
+// instead of sleeping (a sleeping worker's wake-up costs more than widening
+// its share of a band); one per host-buffer call.
+struct Burst {
+    Burst();
+    ~Burst();
+    Burst(const Burst&) = delete;
+    Burst& operator=(const Burst&) = delete;
+};
+
 // dst[i] = (double)src[i] / dst[i] = src[i], parallel over the pool;
 // streaming stores when `stream` (no read-for-ownership of dst).
 void widen(const float* src, double* dst, size_t n, bool stream);
