@@ -76,7 +76,7 @@ def _max_over_ranks(t):
         dist.all_reduce(c, op=dist.ReduceOp.MAX)
         t.copy_(c)
     else:
-        _max_over_ranks(t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t
 
 
@@ -731,9 +731,10 @@ def main() -> None:
                     "pageable_ms_per_step_median": statistics.median(pg_each) * 1e3,
                     "note": "tg_fbm_generate_f64_host (drop-in generate_into span<double>) into pinned host "
                             "memory; input is the config struct only; fp32 bands cross PCIe (64 MiB) and "
-                            "are widened to the caller's doubles by the host pool while later bands are in "
-                            "flight (a measured fraction of bands is widened on the device instead when the "
-                            "host is slower, capi.cu generate_host); pageable_ms: the same call into a "
+                            "are widened to the caller's doubles by the host pool (polling workers, L2 "
+                            "prefetch of the freshly DMA-written band) while later bands are in flight "
+                            "(capi.cu generate_host); bound by PCIe (~1.26 ms) on a quiet host, by the host's "
+                            "reads of the DMA-written bands otherwise; pageable_ms: the same call into a "
                             "pageable buffer"},
             "gpu_launches": K,
             "clocks": clk.summary(),
