@@ -9,6 +9,7 @@
 // Errors map onto terrain/errors.hpp through the tg_status codes.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -661,15 +662,21 @@ int tg_fbm_generate_batch_f32(const tg_fbm_config* cfg, const uint64_t* seeds, i
 // fp32 destination takes the copy directly.  Staging is cached per device.
 namespace {
 
-constexpr int kSlots = 4;
+constexpr int kSlots = 16;
 #ifndef TG_BAND_LOG2
-#define TG_BAND_LOG2 21
+#define TG_BAND_LOG2 20
 #endif
-constexpr size_t kBandElems = size_t(1) << TG_BAND_LOG2;  // 8 MiB of fp32 per band (4 MiB: 1.48 ms, 8: 1.38, 16: 1.7-1.9 at config 2)
+// 4 MiB of fp32 per full band in a ring of 8 slots.  Config 2, f64 drop-in,
+// workers joined asynchronously: 2 MiB bands 1.89-2.03 ms in a 5-slot ring but
+// 1.40-1.45 in 16 slots (a slot rewritten by DMA while its lines still sit in
+// the workers' caches slows both sides), 4 MiB 1.38-1.45 in 8 slots, 8 MiB
+// 1.44-1.54 on a quiet host and 1.96 where the host is the slower side.
+constexpr size_t kBandElems = size_t(1) << TG_BAND_LOG2;
 
 struct HostStage {
     int dev = -1;
     size_t cap = 0;  // elements per band slot
+    int nslots = 0;  // pinned slots allocated
     cudaStream_t st[2] = {nullptr, nullptr};
     float* dbuf[2] = {nullptr, nullptr};
     double* dwide[2] = {nullptr, nullptr};  // device-widened bands (pinned f64 destinations)
@@ -685,9 +692,10 @@ void stage_free_buffers(HostStage* s) {
     for (auto& d : s->dwide) if (d) cudaFree(d), d = nullptr;
     for (auto& p : s->pin) if (p) cudaFreeHost(p), p = nullptr;
     s->cap = 0;
+    s->nslots = 0;
 }
 
-HostStage* stage_acquire(int dev, size_t cap) {
+HostStage* stage_acquire(int dev, size_t cap, int nslots) {
     HostStage* s = nullptr;
     {
         std::lock_guard<std::mutex> lk(g_stage_m);
@@ -710,12 +718,15 @@ HostStage* stage_acquire(int dev, size_t cap) {
             return nullptr;  // leaks the half-built stage; only on a broken device
         }
     }
-    if (s->cap < cap) {
+    if (s->cap < cap || s->nslots < nslots) {
+        cap = std::max(cap, s->cap);
         stage_free_buffers(s);
         bool ok = true;
         for (auto& d : s->dbuf) ok = ok && cudaMalloc(reinterpret_cast<void**>(&d), cap * sizeof(float)) == cudaSuccess;
         for (auto& d : s->dwide) ok = ok && cudaMalloc(reinterpret_cast<void**>(&d), cap * sizeof(double)) == cudaSuccess;
-        for (auto& p : s->pin) ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&p), cap * sizeof(float), cudaHostAllocDefault) == cudaSuccess;
+        for (int k = 0; k < nslots; ++k)
+            ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&s->pin[k]), cap * sizeof(float), cudaHostAllocDefault) == cudaSuccess;
+        s->nslots = nslots;
         if (!ok) {
             cudaGetLastError();
             stage_free_buffers(s);
@@ -768,9 +779,40 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     TG_CUDA(cudaGetDevice(&dev));
 
     const int64_t th = tg::fbm2d_tile_h();
-    int64_t band = std::max<int64_t>(th, static_cast<int64_t>(kBandElems) / extent / th * th);
-    band = std::min<int64_t>(band, extent);
-    const int64_t nb = (extent + band - 1) / band;
+    // full bands: an eighth of the map, between 1 MiB and 8 MiB of fp32
+    const int64_t hi = std::max<int64_t>(th, static_cast<int64_t>(kBandElems) / extent / th * th);
+    const int64_t lo = ((static_cast<int64_t>(kBandElems) / 8 + extent - 1) / extent + th - 1) / th * th;
+    int64_t band = std::min(std::max(extent / 8 / th * th, lo), hi);
+    band = std::min<int64_t>(std::max<int64_t>(band, th), extent);
+    // Band schedule (row counts, whole tile rows): full bands in the middle,
+    // bands of 1, 1, 2, 4, ... tile rows at both ends when the map holds at
+    // least four full bands — the host starts widening after one tile row's
+    // generation + copy instead of a full band's, and the last band's
+    // widening, which nothing overlaps, is one tile row (config 2: 14 bands
+    // instead of 8).
+    std::vector<int64_t> band_h;
+    {
+        std::vector<int64_t> head;
+        if (env_flag("TG_HOST_GRADED", true) && extent >= 4 * band && band >= 2 * th) {
+            head.push_back(th);
+            for (int64_t g = th; g < band; g *= 2) head.push_back(g);
+        }
+        int64_t hsum = 0;
+        for (int64_t g : head) hsum += g;
+        int64_t rest = extent - 2 * hsum;
+        band_h = head;
+        for (; rest >= band; rest -= band) band_h.push_back(band);
+        // the part that fills no band: whole tile rows as one more middle band,
+        // a last partial tile row with the final band
+        const int64_t part = rest / th * th, tail_extra = head.empty() ? 0 : rest - part;
+        if (head.empty() ? rest > 0 : part > 0) band_h.push_back(head.empty() ? rest : part);
+        for (size_t k = head.size(); k-- > 0;) band_h.push_back(head[k]);
+        if (tail_extra) band_h.back() += tail_extra;
+    }
+    const int64_t nb = static_cast<int64_t>(band_h.size());
+    std::vector<int64_t> band_y(band_h.size());
+    for (int64_t k = 0, y = 0; k < nb; y += band_h[k++]) band_y[k] = y;
+    const int64_t band_cap = *std::max_element(band_h.begin(), band_h.end());
     const bool pinned = is_pinned(host_out);
     const bool direct32 = !f64 && pinned;  // fp32 into pinned: one DMA per band
     // f64 destinations: bands cross PCIe as fp32 (4 B/sample) into the pinned
@@ -794,41 +836,54 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
         return std::floor(static_cast<double>(i + 1) * frac) > std::floor(static_cast<double>(i) * frac);
     };
     const bool nt = env_flag("TG_HOST_STREAM_STORES", true);
-    HostStage* s = stage_acquire(dev, static_cast<size_t>(band) * static_cast<size_t>(extent));
-    if (!s) return fail(TG_EDEVICE, "generate: staging allocation failed");
 
     int rc = TG_OK;
-    constexpr int ns = kSlots;  // a ring as deep as the map (DMA never throttled) measured the same
+    // ring of ns staging slots (TG_HOST_SLOTS, default 8): kLook bands
+    // generated / copied ahead of the one the pool is widening, one slot being
+    // widened, one whose widening the next submission joins.  The depth keeps
+    // a slot from being rewritten by DMA while its lines are still in the
+    // workers' caches.
+    const int ns = std::min(kSlots, std::max(3, static_cast<int>(env_double("TG_HOST_SLOTS", 8))));
+    const int kLook = std::min(ns - 2, std::max(1, static_cast<int>(env_double("TG_HOST_LOOK", ns - 2))));
+    HostStage* s = stage_acquire(dev, static_cast<size_t>(band_cap) * static_cast<size_t>(extent), ns);
+    if (!s) return fail(TG_EDEVICE, "generate: staging allocation failed");
     const bool dbg = env_flag("TG_HOST_DEBUG", false);
     // workers poll between bands for the length of this call (direct fp32
     // DMA into a pinned destination has no host work)
     std::unique_ptr<tg::host::Burst> burst;
     if (!direct32 && env_flag("TG_HOST_SPIN", true)) burst.reset(new tg::host::Burst);
+    // The pool widens band j while this thread queues the device work of the
+    // bands after it (launch + copy + event: ~15 us per band that used to sit
+    // on the host-bound critical path); a submission first joins the previous
+    // band's job, so a slot's widening is complete two submissions later,
+    // before its slot is copied into again.
+    tg::host::Pending pending;
     auto drain = [&](int64_t j) {
         const int slot = static_cast<int>(j % ns);
         const auto tw0 = std::chrono::steady_clock::now();
         if (cudaError_t e = cudaEventSynchronize(s->ev[slot])) {
             if (rc == TG_OK) rc = cuda_fail(e, "generate_host");
+            pending.wait();
             return;
         }
-        if (direct32 || rc != TG_OK || (f64 && !host_widened(j))) return;
-        const int64_t y0 = j * band, h = std::min<int64_t>(band, extent - y0);
-        const size_t n = static_cast<size_t>(h) * static_cast<size_t>(extent);
-        const size_t off = static_cast<size_t>(y0) * static_cast<size_t>(extent);
-        if (f64) {
-            const auto t0 = std::chrono::steady_clock::now();
-            tg::host::widen(s->pin[slot], static_cast<double*>(host_out) + off, n, nt);
-            if (dbg)  // TG_HOST_DEBUG=1: per band, the wait for its copy and the widening time
-                std::fprintf(stderr, "band %lld wait %.1f us widen %.1f us\n", static_cast<long long>(j),
-                             std::chrono::duration<double, std::micro>(t0 - tw0).count(),
-                             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+        if (direct32 || rc != TG_OK || (f64 && !host_widened(j))) {
+            pending.wait();
+            return;
         }
-        else tg::host::copy(s->pin[slot], static_cast<float*>(host_out) + off, n, nt);
+        const size_t n = static_cast<size_t>(band_h[j]) * static_cast<size_t>(extent);
+        const size_t off = static_cast<size_t>(band_y[j]) * static_cast<size_t>(extent);
+        const auto t0 = std::chrono::steady_clock::now();
+        if (f64) pending = tg::host::widen_async(s->pin[slot], static_cast<double*>(host_out) + off, n, nt);
+        else pending = tg::host::copy_async(s->pin[slot], static_cast<float*>(host_out) + off, n, nt);
+        if (dbg)  // TG_HOST_DEBUG=1: per band, the wait for its copy and the join of the previous band's job
+            std::fprintf(stderr, "band %lld rows %lld wait %.1f us join+submit %.1f us\n", static_cast<long long>(j),
+                         static_cast<long long>(band_h[j]), std::chrono::duration<double, std::micro>(t0 - tw0).count(),
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     };
     tg::FbmArgs a;
     int64_t issued = 0;
     for (int64_t i = 0; i < nb && rc == TG_OK; ++i) {
-        const int64_t y0 = i * band, h = std::min<int64_t>(band, extent - y0);
+        const int64_t y0 = band_y[i], h = band_h[i];
         const int b = static_cast<int>(i & 1), slot = static_cast<int>(i % ns);
         if (build_args(cfg, ox, oy + y0, extent, h, extent, &a) != TG_OK) {
             rc = TG_EDEVICE;
@@ -854,9 +909,10 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
             break;
         }
         issued = i + 1;
-        if (i >= ns - 1) drain(i - (ns - 1));
+        if (i >= kLook) drain(i - kLook);
     }
-    for (int64_t j = std::max<int64_t>(0, issued - (ns - 1)); j < issued; ++j) drain(j);
+    for (int64_t j = std::max<int64_t>(0, issued - kLook); j < issued; ++j) drain(j);
+    pending.wait();
     for (auto st : s->st) {
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess && rc == TG_OK) rc = cuda_fail(e, "generate_host sync");

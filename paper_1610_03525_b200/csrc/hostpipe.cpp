@@ -45,45 +45,62 @@ class Pool {
     }
     void end_burst() { hot_.fetch_sub(1, std::memory_order_release); }
 
-    void run(int n, const std::function<void(int)>& f) {
-        std::lock_guard<std::mutex> submit(submit_);
-        if (n_ <= 1 || n <= 1) {
-            for (int i = 0; i < n; ++i) f(i);
-            return;
-        }
+    // One submission.  A worker that wakes late holds an old job, whose index
+    // counter is exhausted, so it can never run a stale function.
+    struct Job {
+        std::function<void(int)> fn;
+        int total = 0;
+        std::atomic<int> next{0}, done{0};
+    };
+    using Handle = std::shared_ptr<Job>;
+
+    // Publishes f(0..n-1) to the workers and returns at once; the caller
+    // joins it with finish().  The pool runs one job at a time: submitting
+    // first completes (helping) whichever job is current, so a caller's jobs
+    // finish in submission order.  Submissions from different threads
+    // interleave job by job.
+    Handle submit(int n, std::function<void(int)> f) {
         auto job = std::make_shared<Job>();
-        job->fn = &f;
+        job->fn = std::move(f);
         job->total = n;
+        if (n_ <= 1 || n <= 1) {
+            for (int i = 0; i < n; ++i) job->fn(i);
+            job->done.store(n);
+            return job;
+        }
+        std::lock_guard<std::mutex> submit(submit_);
+        if (cur_) complete(*cur_);
         {
             std::lock_guard<std::mutex> lk(m_);
             job_ = job;
             gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
-        work(*job);
+        cur_ = job;
+        return job;
+    }
+    void finish(const Handle& h) {
+        if (h && h->done.load(std::memory_order_acquire) != h->total) complete(*h);
+    }
+    void run(int n, const std::function<void(int)>& f) { finish(submit(n, f)); }
+
+   private:
+    // help with the job's remaining pieces, then wait for the stragglers
+    void complete(Job& j) {
+        work(j);
         if (hot_.load(std::memory_order_acquire) > 0) {
-            // the stragglers are mid-piece: poll, they finish within microseconds
-            for (int spins = 0; job->done.load(std::memory_order_acquire) != n && spins < (1 << 22); ++spins)
+            // mid-piece workers finish within microseconds: poll
+            for (int spins = 0; j.done.load(std::memory_order_acquire) != j.total && spins < (1 << 22); ++spins)
                 _mm_pause();
         }
         std::unique_lock<std::mutex> lk(m_);
-        done_cv_.wait(lk, [&] { return job->done.load() == n; });
-        job_.reset();
+        done_cv_.wait(lk, [&] { return j.done.load() == j.total; });
     }
-
-   private:
-    // One submission; a worker that wakes late holds the old job, whose index
-    // counter is exhausted, so it can never run a stale function.
-    struct Job {
-        const std::function<void(int)>* fn = nullptr;
-        int total = 0;
-        std::atomic<int> next{0}, done{0};
-    };
 
     void work(Job& j) {
         int i, mine = 0;
         while ((i = j.next.fetch_add(1)) < j.total) {
-            (*j.fn)(i);
+            j.fn(i);
             ++mine;
         }
         if (mine && j.done.fetch_add(mine) + mine == j.total) {
@@ -116,7 +133,8 @@ class Pool {
     int n_;
     std::mutex submit_, m_;
     std::condition_variable cv_, done_cv_;
-    std::shared_ptr<Job> job_;
+    std::shared_ptr<Job> job_;  // published to the workers (under m_)
+    std::shared_ptr<Job> cur_;  // last submitted (under submit_)
     std::atomic<uint64_t> gen_{0};
     std::atomic<int> hot_{0};
 };
@@ -152,8 +170,13 @@ __attribute__((target("avx512f"))) void widen_avx512(const float* s, double* d, 
     // still running; an L2 prefetch 16 KiB ahead does (B200 host, config 2,
     // 6 workers: 2.2 -> 2.0 ms; 10 workers 1.93 -> 1.80 ms).
     static const int pf = [] { const char* e = std::getenv("TG_HOST_PREFETCH"); return e ? std::atoi(e) : 16384; }();
+    static const int hint = [] { const char* e = std::getenv("TG_HOST_PREFETCH_HINT"); return e ? std::atoi(e) : 0; }();
     for (; i + 16 <= n; i += 16) {
-        if (pf) _mm_prefetch(reinterpret_cast<const char*>(s + i) + pf, _MM_HINT_T1);
+        if (pf) {
+            if (hint == 1) _mm_prefetch(reinterpret_cast<const char*>(s + i) + pf, _MM_HINT_NTA);
+            else if (hint == 2) _mm_prefetch(reinterpret_cast<const char*>(s + i) + pf, _MM_HINT_T0);
+            else _mm_prefetch(reinterpret_cast<const char*>(s + i) + pf, _MM_HINT_T1);
+        }
         const __m512 a = _mm512_loadu_ps(s + i);
         _mm512_stream_pd(d + i, _mm512_cvtps_pd(_mm512_castps512_ps256(a)));
         _mm512_stream_pd(d + i + 8, _mm512_cvtps_pd(_mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castps_pd(a), 1))));
@@ -207,18 +230,19 @@ void copy_serial(const float* s, float* d, size_t n, bool stream) {
 #endif
 constexpr size_t kPiecesPerWorker = TG_HOST_PIECES;
 
+// n elements in pieces of >= 64 KiB of input on 64-element boundaries, a few
+// pieces per worker (dynamic hand-out): a worker that starts late or shares
+// its core does not hold the whole band back.  f(begin, count) is copied
+// into the job.
 template <class F>
-void split(size_t n, F&& f) {
+Pool::Handle split(size_t n, F f) {
     const int t = pool().size();
-    // >= 64 KiB of input per piece, pieces on 64-element boundaries
     const size_t min_piece = 16384;
-    // a few pieces per worker (dynamic hand-out): a worker that starts late
-    // or shares its core does not hold the whole band back
     int pieces = static_cast<int>(std::min<size_t>(static_cast<size_t>(t) * kPiecesPerWorker, (n + min_piece - 1) / min_piece));
     pieces = std::max(pieces, 1);
     size_t per = (n + pieces - 1) / pieces;
     per = (per + 63) / 64 * 64;
-    pool().run(pieces, [&](int k) {
+    return pool().submit(pieces, [f, per, n](int k) {
         const size_t b = static_cast<size_t>(k) * per;
         if (b >= n) return;
         f(b, std::min(per, n - b));
@@ -234,13 +258,39 @@ Burst::~Burst() { pool().end_burst(); }
 
 void parallel_for(int n, const std::function<void(int)>& f) { pool().run(n, f); }
 
-void widen(const float* src, double* dst, size_t n, bool stream) {
-    split(n, [&](size_t b, size_t m) { widen_serial(src + b, dst + b, m, stream); });
+struct Pending::Impl {
+    std::shared_ptr<void> h;  // Pool::Handle
+};
+Pending::Pending() = default;
+Pending::~Pending() { wait(); }
+Pending::Pending(Pending&& o) noexcept : impl_(std::move(o.impl_)) {}
+Pending& Pending::operator=(Pending&& o) noexcept {
+    if (this != &o) {
+        wait();
+        impl_ = std::move(o.impl_);
+    }
+    return *this;
+}
+void Pending::wait() {
+    if (impl_) pool().finish(std::static_pointer_cast<Pool::Job>(impl_->h));
+    impl_.reset();
 }
 
-void copy(const float* src, float* dst, size_t n, bool stream) {
-    split(n, [&](size_t b, size_t m) { copy_serial(src + b, dst + b, m, stream); });
+Pending widen_async(const float* src, double* dst, size_t n, bool stream) {
+    Pending p;
+    p.impl_.reset(new Pending::Impl{split(n, [=](size_t b, size_t m) { widen_serial(src + b, dst + b, m, stream); })});
+    return p;
 }
+
+Pending copy_async(const float* src, float* dst, size_t n, bool stream) {
+    Pending p;
+    p.impl_.reset(new Pending::Impl{split(n, [=](size_t b, size_t m) { copy_serial(src + b, dst + b, m, stream); })});
+    return p;
+}
+
+void widen(const float* src, double* dst, size_t n, bool stream) { widen_async(src, dst, n, stream).wait(); }
+
+void copy(const float* src, float* dst, size_t n, bool stream) { copy_async(src, dst, n, stream).wait(); }
 
 }  // namespace host
 }  // namespace tg

@@ -5,6 +5,7 @@
 #pragma once
 #include <cstddef>
 #include <functional>
+#include <memory>
 
 namespace tg {
 namespace host {
@@ -31,6 +32,27 @@ struct Burst {
 // streaming stores when `stream` (no read-for-ownership of dst).
 void widen(const float* src, double* dst, size_t n, bool stream);
 void copy(const float* src, float* dst, size_t n, bool stream);
+
+// The same, returning at once: the pool's workers start on the band while the
+// caller queues the next band's device work; wait() (or the destructor, or
+// the next submission) joins it, the caller helping with what is left.  A
+// caller's submissions complete in order.
+class Pending {
+   public:
+    Pending();
+    ~Pending();
+    Pending(Pending&&) noexcept;
+    Pending& operator=(Pending&&) noexcept;
+    void wait();
+
+   private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+    friend Pending widen_async(const float*, double*, size_t, bool);
+    friend Pending copy_async(const float*, float*, size_t, bool);
+};
+Pending widen_async(const float* src, double* dst, size_t n, bool stream);
+Pending copy_async(const float* src, float* dst, size_t n, bool stream);
 
 }  // namespace host
 }  // namespace tg
