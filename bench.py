@@ -731,10 +731,9 @@ def main() -> None:
                     "pageable_ms_per_step_median": statistics.median(pg_each) * 1e3,
                     "note": "tg_fbm_generate_f64_host (drop-in generate_into span<double>) into pinned host "
                             "memory; input is the config struct only; fp32 bands cross PCIe (64 MiB) and "
-                            "are widened to the caller's doubles by the host pool (polling workers, L2 "
-                            "prefetch of the freshly DMA-written band) while later bands are in flight "
-                            "(capi.cu generate_host); bound by PCIe (~1.26 ms) on a quiet host, by the host's "
-                            "reads of the DMA-written bands otherwise; pageable_ms: the same call into a "
+                            "are widened to the caller's doubles by the host pool inside the copies' shadow "
+                            "(4 MiB bands, 8-slot pinned ring, asynchronous pool join; capi.cu generate_host); "
+                            "the PCIe time of the 64 MiB is ~1.26 ms; pageable_ms: the same call into a "
                             "pageable buffer"},
             "gpu_launches": K,
             "clocks": clk.summary(),
