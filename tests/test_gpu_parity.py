@@ -212,7 +212,7 @@ def test_host_drop_in_matches_device():
 
 @pytest.mark.parametrize("frac", ["0", "0.5", "1"])
 def test_host_pipeline_bands_pinned_pageable(frac, monkeypatch):
-    """Banded host path: 10 ragged bands through the 4-slot staging ring, f64
+    """Banded host path: ragged, graded bands through the staging ring, f64
     (device- and host-widened mixes) and f32 destinations, pinned, pageable
     and misaligned (streaming-store head) buffers."""
     monkeypatch.setenv("TG_HOST_WIDEN_FRAC", frac)
@@ -227,6 +227,48 @@ def test_host_pipeline_bands_pinned_pageable(frac, monkeypatch):
                 view = t[off:off + E * E]
                 pt.generate_into(cfg, (0, 0), E, view.numpy())
                 assert torch.equal(view.view(E, E), want), (dt, pinned, off)
+
+
+def test_host_pipeline_concurrent_callers_and_schedules(monkeypatch):
+    """The asynchronous pool join under contention: four host threads call the
+    drop-in at once (ctypes drops the GIL) with different seeds and extents;
+    every result equals the device map.  Then the band schedule knobs
+    (ungraded bands, shallow / deep rings) give the same bytes."""
+    import threading
+
+    cases = [(seed, E) for seed, E in ((3, 1024), (4, 1500), (5, 2048), (6, 777))]
+    cfgs = {seed: pt.FbmConfig(seed=seed, resolution=4096, base_frequency=8, octaves=12, smoothstep=5)
+            for seed, _ in cases}
+    want = {seed: gen(cfgs[seed].to_c(), 0, 0, E).cpu().to(torch.float64) for seed, E in cases}
+    outs = {seed: torch.full((E, E), -3.0, dtype=torch.float64, pin_memory=(seed % 2 == 0)) for seed, E in cases}
+    errs = []
+
+    def work(seed, E):
+        try:
+            for _ in range(6):
+                outs[seed].fill_(-3.0)
+                pt.generate_into(cfgs[seed], (0, 0), E, outs[seed].numpy())
+                if not torch.equal(outs[seed], want[seed]):
+                    errs.append((seed, "mismatch"))
+        except Exception as e:  # pragma: no cover
+            errs.append((seed, repr(e)))
+
+    th = [threading.Thread(target=work, args=c) for c in cases]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    seed, E = 5, 2048
+    for env in ({"TG_HOST_GRADED": "0"}, {"TG_HOST_SLOTS": "3"}, {"TG_HOST_SLOTS": "16", "TG_HOST_LOOK": "2"},
+                {"TG_HOST_SPIN": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        outs[seed].fill_(-3.0)
+        pt.generate_into(cfgs[seed], (0, 0), E, outs[seed].numpy())
+        assert torch.equal(outs[seed], want[seed]), env
+        for k in env:
+            monkeypatch.delenv(k)
 
 
 def test_validation_errors_on_device_path():
