@@ -779,9 +779,14 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     TG_CUDA(cudaGetDevice(&dev));
 
     const int64_t th = tg::fbm2d_tile_h();
-    // full bands: an eighth of the map, between 1 MiB and 8 MiB of fp32
-    const int64_t hi = std::max<int64_t>(th, static_cast<int64_t>(kBandElems) / extent / th * th);
-    const int64_t lo = ((static_cast<int64_t>(kBandElems) / 8 + extent - 1) / extent + th - 1) / th * th;
+    const bool pinned = is_pinned(host_out);
+    const bool direct32 = !f64 && pinned;  // fp32 into pinned: one DMA per band
+    // full bands: an eighth of the map, between 0.5 MiB and 4 MiB of fp32 (8 MiB
+    // when the band is DMA'd straight into the destination: larger copies
+    // move 2 % faster and no host work hides behind them)
+    const int64_t band_elems = static_cast<int64_t>(direct32 ? 2 * kBandElems : kBandElems);
+    const int64_t hi = std::max<int64_t>(th, band_elems / extent / th * th);
+    const int64_t lo = ((band_elems / 8 + extent - 1) / extent + th - 1) / th * th;
     int64_t band = std::min(std::max(extent / 8 / th * th, lo), hi);
     band = std::min<int64_t>(std::max<int64_t>(band, th), extent);
     // Band schedule (row counts, whole tile rows): full bands in the middle,
@@ -813,8 +818,6 @@ static int generate_host(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int64
     std::vector<int64_t> band_y(band_h.size());
     for (int64_t k = 0, y = 0; k < nb; y += band_h[k++]) band_y[k] = y;
     const int64_t band_cap = *std::max_element(band_h.begin(), band_h.end());
-    const bool pinned = is_pinned(host_out);
-    const bool direct32 = !f64 && pinned;  // fp32 into pinned: one DMA per band
     // f64 destinations: bands cross PCIe as fp32 (4 B/sample) into the pinned
     // staging ring and the host pool widens them into the caller's buffer
     // while later bands are in flight.  With a pinned destination a fraction
