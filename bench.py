@@ -53,6 +53,28 @@ BYTES_PER_SAMPLE = 4         # one fp32 store per sample, no inputs
 SHARED_GPU = os.environ.get("TG_BENCH_SHARED_GPU", "0") == "1"
 
 
+# The contract is ONE JSON line on stdout.  Libraries write there too (NCCL
+# prints "NCCL version ..." on stdout when its first communicator comes up), so
+# file descriptor 1 is pointed at stderr for the life of the process and the
+# line goes out through a duplicate of the original stdout.
+_REAL_STDOUT = None
+
+
+def _own_stdout() -> None:
+    global _REAL_STDOUT
+    if _REAL_STDOUT is None:
+        sys.stdout.flush()
+        _REAL_STDOUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+        sys.stdout = sys.stderr
+
+
+def _emit(line: dict) -> None:
+    out = _REAL_STDOUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def _device_index(local: int) -> int:
     return 0 if SHARED_GPU else local
 
@@ -420,7 +442,7 @@ def run_reference_arm(args, rank: int, world: int) -> None:
                          "sample": sample},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 def run_cfg5_workload(args, rank: int, world: int, local: int) -> None:
@@ -518,7 +540,7 @@ def run_cfg5_workload(args, rank: int, world: int, local: int) -> None:
             "gpu_launches": K, "clocks": clk.summary(), "cpu_baseline": None,
             "cfg5_terrain": stats,
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -538,6 +560,7 @@ def main() -> None:
                          "in N row bands (strong scaling) with NCCL-reduced statistics")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 terrain section of the cfg2 line")
     args = ap.parse_args()
+    _own_stdout()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -741,7 +764,7 @@ def main() -> None:
             "analysis": analysis,
             "cfg5_terrain": terrain5,
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -74,3 +74,39 @@ def test_bench_nccl_helpers_one_rank(tmp_path):
     out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "ok" in out.stdout
+
+
+REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "e2e")
+
+
+def _one_json_line(stdout: str) -> dict:
+    import json
+
+    lines = [ln for ln in stdout.split("\n") if ln.strip()]
+    assert len(lines) == 1, f"stdout must hold exactly one line, got {len(lines)}: {stdout[:300]!r}"
+    return json.loads(lines[0])
+
+
+def test_reference_arm_prints_one_json_line():
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtgref.so")):
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = _one_json_line(out.stdout)
+    assert d["impl"] == "reference" and all(k in d for k in REQUIRED) and "cpu_baseline" in d
+
+
+@pytest.mark.gpu
+def test_bench_prints_one_json_line_with_the_contract_keys():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "5", "--warmup", "3",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = _one_json_line(out.stdout)  # NCCL's version banner must not land on stdout
+    assert all(k in d for k in REQUIRED + ("roofline", "gpu_launches", "clocks"))
+    assert d["gpu_launches"] == 5 and d["e2e"]["d2h_bytes_per_step"] == 4096 * 4096 * 8
+    assert d["cfg5_terrain"] and "error" not in d["cfg5_terrain"]
