@@ -130,45 +130,6 @@ __global__ void radix_hist2d(const float* __restrict__ x, int64_t width, int64_t
     hist_flush(sh, hist);
 }
 
-// Picks the digit whose cumulative count crosses the remaining rank k
-// (one block of kBins / 2 threads, two bins each), then clears the histogram
-// for the next pass.
-__global__ void __launch_bounds__(kBins / 2) radix_pick(SelectState* st, unsigned long long* hist, int shift, int bits) {
-    __shared__ unsigned long long wsum[32];
-    const int nb = 1 << bits, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const unsigned long long h0 = 2 * t < nb ? hist[2 * t] : 0, h1 = 2 * t + 1 < nb ? hist[2 * t + 1] : 0;
-    unsigned long long inc = h0 + h1;  // inclusive scan over threads
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-    }
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        unsigned long long w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long v = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += v;
-        }
-        wsum[lane] = w;
-    }
-    __syncthreads();
-    const unsigned long long before = inc - h0 - h1 + (warp ? wsum[warp - 1] : 0);
-    const uint64_t k = st->k;
-    int b = -1;
-    unsigned long long acc = 0;
-    if (before <= k && k < before + h0) b = 2 * t, acc = before;
-    else if (before + h0 <= k && k < before + h0 + h1) b = 2 * t + 1, acc = before + h0;
-    __syncthreads();  // every thread has read st->k
-    if (b >= 0) {
-        st->k = k - acc;
-        st->prefix |= static_cast<uint32_t>(b) << shift;
-        st->mask |= static_cast<uint32_t>(nb - 1) << shift;
-    }
-    if (2 * t < kBins) hist[2 * t] = 0;
-    if (2 * t + 1 < kBins) hist[2 * t + 1] = 0;
-}
-
 // ---- radix select with a sampled candidate window -----------------------------
 // Three full histogram passes cost three reads of the map.  Instead the first
 // pass also compacts every key whose first digit lies in a window of digits

@@ -553,9 +553,9 @@ int tg_fbm_octave_times(const tg_fbm_config* cfg, int64_t ox, int64_t oy, int32_
     int dev = 0;
     cudaGetDevice(&dev);
     char keyb[256];
-    snprintf(keyb, sizeof(keyb), "%d|%d|%d|%d|%lld|%d|%.17g|%.17g|%.17g|%d|%d", dev, cfg->method, cfg->smoothstep,
+    snprintf(keyb, sizeof(keyb), "%d|%d|%d|%d|%lld|%d|%.17g|%.17g|%.17g|%d|%lld", dev, cfg->method, cfg->smoothstep,
              cfg->octaves, static_cast<long long>(cfg->resolution), cfg->base_frequency, cfg->frequency_ratio,
-             cfg->persistence, cfg->base_amplitude, cfg->zero_lattice, extent);
+             cfg->persistence, cfg->base_amplitude, cfg->zero_lattice, static_cast<long long>(extent));
     {
         std::lock_guard<std::mutex> lock(mu);
         auto it = cache.find(keyb);

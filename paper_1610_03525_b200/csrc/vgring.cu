@@ -77,8 +77,6 @@ struct WalkPlan {
     int64_t hw[3];
 };
 
-__device__ __forceinline__ int top_m(uint32_t mask) { return mask ? 1 << (31 - __clz(mask)) : 0; }
-
 __device__ __forceinline__ int clamp_step(int64_t v) {
     return static_cast<int>(v < -(int64_t(1) << 30) ? -(int64_t(1) << 30) : v > (int64_t(1) << 30) ? (int64_t(1) << 30) : v);
 }
@@ -313,7 +311,7 @@ template <int KIND, bool ALL>
 __global__ void __launch_bounds__(kThreads, TG_VGR_MINB)
 vg_walk(const float* __restrict__ z, int64_t W, int64_t ld, int64_t P, bool vec, const __grid_constant__ RingPlan plan,
         const __grid_constant__ WalkPlan wp, double* __restrict__ sums) {
-    constexpr int AX = KIND >= kY0 ? 1 : 0, C = KIND % 3, NM = C == 2 ? 3 : 5, OFF = C == 0 ? 0 : C == 1 ? 5 : 10;
+    constexpr int AX = KIND >= kY0 ? 1 : 0, C = KIND % 3, NM = C == 2 ? 3 : 5;
     __shared__ double part_s[kWarps][8];
     extern __shared__ __align__(16) float stage_s[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
