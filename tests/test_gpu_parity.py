@@ -212,7 +212,7 @@ def test_host_drop_in_matches_device():
 
 @pytest.mark.parametrize("frac", ["0", "0.5", "1"])
 def test_host_pipeline_bands_pinned_pageable(frac, monkeypatch):
-    """Banded host path: ragged, graded bands through the staging ring, f64
+    """Banded host path: ragged bands through the staging ring, f64
     (device- and host-widened mixes) and f32 destinations, pinned, pageable
     and misaligned (streaming-store head) buffers."""
     monkeypatch.setenv("TG_HOST_WIDEN_FRAC", frac)
@@ -233,7 +233,7 @@ def test_host_pipeline_concurrent_callers_and_schedules(monkeypatch):
     """The asynchronous pool join under contention: four host threads call the
     drop-in at once (ctypes drops the GIL) with different seeds and extents;
     every result equals the device map.  Then the band schedule knobs
-    (ungraded bands, shallow / deep rings) give the same bytes."""
+    (small / large bands, shallow / deep rings) give the same bytes."""
     import threading
 
     cases = [(seed, E) for seed, E in ((3, 1024), (4, 1500), (5, 2048), (6, 777))]
@@ -260,8 +260,8 @@ def test_host_pipeline_concurrent_callers_and_schedules(monkeypatch):
         t.join()
     assert not errs, errs
     seed, E = 5, 2048
-    for env in ({"TG_HOST_GRADED": "0"}, {"TG_HOST_SLOTS": "3"}, {"TG_HOST_SLOTS": "16", "TG_HOST_LOOK": "2"},
-                {"TG_HOST_SPIN": "0"}):
+    for env in ({"TG_HOST_BAND_LOG2": "17"}, {"TG_HOST_BAND_LOG2": "23"}, {"TG_HOST_SLOTS": "3"},
+                {"TG_HOST_SLOTS": "16", "TG_HOST_LOOK": "2"}, {"TG_HOST_SPIN": "0"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         outs[seed].fill_(-3.0)
