@@ -14,6 +14,16 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
 GLOO_CHILD = textwrap.dedent("""
     import os, sys
     sys.path.insert(0, %r)
@@ -35,7 +45,7 @@ def test_max_over_ranks_gloo_two_ranks(tmp_path):
     script.write_text(GLOO_CHILD)
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                          "--master-addr", "127.0.0.1", "--master-port", "29631", str(script)],
+                          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(script)],
                          capture_output=True, text=True, env=env, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.count("ok") == 2
@@ -44,7 +54,8 @@ def test_max_over_ranks_gloo_two_ranks(tmp_path):
 NCCL_CHILD = textwrap.dedent("""
     import os, sys
     sys.path.insert(0, %r)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29632", RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ["TG_TEST_PORT"], RANK="0", WORLD_SIZE="1",
+                      LOCAL_RANK="0")
     os.environ.pop("TG_BENCH_SHARED_GPU", None)
     import torch, torch.distributed as dist
     import bench
@@ -71,7 +82,8 @@ def test_bench_nccl_helpers_one_rank(tmp_path):
         pytest.skip("no CUDA device")
     script = tmp_path / "child.py"
     script.write_text(NCCL_CHILD)
-    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ, TG_TEST_PORT=str(_free_port())))
     assert out.returncode == 0, out.stderr[-2000:]
     assert "ok" in out.stdout
 
