@@ -127,7 +127,10 @@ bool linear_fit(const std::vector<double>& xs, const std::vector<double>& ys, do
 }
 
 int allreduce(tg_comm* c, void* buf, uint64_t count, int dtype, int op) {
-    if (!c || count == 0) return TG_OK;
+    // one rank: the reduction is the identity (the driver skips the six
+    // host -> device -> NCCL -> host round trips of a one-band terrain;
+    // tg_comm_allreduce itself still reduces on a 1-rank communicator)
+    if (!c || count == 0 || c->nranks <= 1) return TG_OK;
     return tg_comm_allreduce(c, buf, count, dtype, op);
 }
 
