@@ -141,17 +141,18 @@ class Pool {
 
 Pool& pool() {
     static Pool* p = [] {
-        // Streaming widen/copy: workers are bound by the latency of reading
-        // the freshly DMA-written bands, so more of them help up to about
-        // half the hardware threads (B200 host, 16 threads, config 2 f64
-        // drop-in with DMA in flight: 4 workers 2.86 ms, 6: 2.29-2.69, 8:
-        // 2.07-2.53, 10: 1.93-2.37; the rest stay free for the CUDA driver
-        // and the caller).  Shared among the ranks of this node
-        // (LOCAL_WORLD_SIZE, set by torchrun), at most 8.
+        // Streaming widen/copy: the workers are bound by the host's memory
+        // system (reads of freshly DMA-written bands, streaming stores), so
+        // more of them help up to a little over half the hardware threads
+        // (16-thread B200 hosts, config 2 f64 drop-in: on the slower hosts of
+        // the pool 6 workers 1.99 ms, 8: 1.87, 10: 1.80-1.83, 12 / 15: 1.83;
+        // on the faster ones 1.34-1.39 ms from 6 workers up); the rest stay
+        // free for the CUDA driver and the caller.  Shared among the ranks of
+        // this node (LOCAL_WORLD_SIZE, set by torchrun), at most 10.
         int n = static_cast<int>(std::thread::hardware_concurrency());
         int ranks = 1;
         if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, std::atoi(e));
-        n = std::min(std::max((n / 2) / ranks, 1), 8);
+        n = std::min(std::max((n * 5 / 8) / ranks, 1), 10);
         if (const char* e = std::getenv("TG_HOST_THREADS")) n = std::max(1, std::atoi(e));
         return new Pool(n);
     }();
