@@ -63,9 +63,13 @@ _REAL_STDOUT = None
 def _own_stdout() -> None:
     global _REAL_STDOUT
     if _REAL_STDOUT is None:
-        sys.stdout.flush()
-        _REAL_STDOUT = os.fdopen(os.dup(1), "w")
-        os.dup2(2, 1)
+        try:
+            sys.stdout.flush()
+            real = os.fdopen(os.dup(1), "w")
+            os.dup2(2, 1)
+        except OSError:  # no usable stderr: leave stdout as it is
+            return
+        _REAL_STDOUT = real
         sys.stdout = sys.stderr
 
 
