@@ -186,6 +186,30 @@ __attribute__((target("avx512f"))) void widen_avx512(const float* s, double* d, 
     _mm_sfence();
 }
 
+// AVX2 form for hosts without AVX-512: 8 floats -> two 32-byte non-temporal
+// stores, the same L2 prefetch ahead of the loads.
+__attribute__((target("avx2"))) void widen_avx2(const float* s, double* d, size_t n) {
+    size_t i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = s[i];
+    static const int pf = [] { const char* e = std::getenv("TG_HOST_PREFETCH"); return e ? std::atoi(e) : 16384; }();
+    for (; i + 8 <= n; i += 8) {
+        if (pf && (i & 15) == 0) _mm_prefetch(reinterpret_cast<const char*>(s + i) + pf, _MM_HINT_T1);
+        const __m256 a = _mm256_loadu_ps(s + i);
+        _mm256_stream_pd(d + i, _mm256_cvtps_pd(_mm256_castps256_ps128(a)));
+        _mm256_stream_pd(d + i + 4, _mm256_cvtps_pd(_mm256_extractf128_ps(a, 1)));
+    }
+    for (; i < n; ++i) d[i] = s[i];
+    _mm_sfence();
+}
+
+bool have_avx2() {
+    static const bool v = [] {
+        if (const char* e = std::getenv("TG_HOST_AVX2")) return std::atoi(e) != 0;
+        return __builtin_cpu_supports("avx2") != 0;
+    }();
+    return v;
+}
+
 bool have_avx512() {
     static const bool v = [] {
         if (const char* e = std::getenv("TG_HOST_AVX512")) return std::atoi(e) != 0;
@@ -196,6 +220,7 @@ bool have_avx512() {
 
 void widen_serial(const float* s, double* d, size_t n, bool stream) {
     if (stream && have_avx512()) return widen_avx512(s, d, n);
+    if (stream && have_avx2()) return widen_avx2(s, d, n);
     size_t i = 0;
     if (stream) {
         for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = s[i];

@@ -31,9 +31,11 @@ def test_hostpipe(binary, threads):
     assert r.stdout.strip().endswith("ok")
 
 
-def test_hostpipe_without_avx512(binary):
+@pytest.mark.parametrize("isa", [{"TG_HOST_AVX512": "0"}, {"TG_HOST_AVX512": "0", "TG_HOST_AVX2": "0"}])
+def test_hostpipe_without_avx512(binary, isa):
+    """The AVX2 and SSE2 widening forms (hosts without AVX-512)."""
     r = subprocess.run([binary], capture_output=True, text=True, timeout=300,
-                       env=dict(os.environ, TG_HOST_AVX512="0", TG_HOST_THREADS="4"))
+                       env=dict(os.environ, TG_HOST_THREADS="4", **isa))
     assert r.returncode == 0, r.stdout + r.stderr
 
 
